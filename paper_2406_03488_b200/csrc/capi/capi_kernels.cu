@@ -1,0 +1,92 @@
+// extern "C" kernel-level entry points (tests, microbenchmarks, bench roofline).
+#include "capi/capi_common.hpp"
+#include "cuda/common.cuh"
+#include "cuda/ops.h"
+#include "seqpipe_b200.h"
+
+namespace {
+spk::DType dt(int32_t d) {
+  if (d != SP_DTYPE_F32 && d != SP_DTYPE_BF16) throw std::invalid_argument("dtype must be SP_DTYPE_F32 or SP_DTYPE_BF16");
+  return d == SP_DTYPE_F32 ? spk::DType::kF32 : spk::DType::kBF16;
+}
+
+template <typename F>
+int cuda_guard(F&& f) {
+  try {
+    f();
+    return SP_OK;
+  } catch (const spk::CudaError& e) {
+    spc::set_error(e.what());
+    return SP_ERR_CUDA;
+  } catch (...) {
+    return spc::map_exception();
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int sp_gemm(int32_t dtype, int32_t impl, const void* A, int32_t a_kmajor, const void* B, int32_t b_kmajor, void* C,
+            int32_t c_f32, int32_t accumulate, int64_t M, int64_t N, int64_t K, void* stream) {
+  return cuda_guard([&] {
+    spk::GemmArgs g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.ab = dt(dtype);
+    g.A = A;
+    g.a_kmajor = a_kmajor != 0;
+    g.lda = a_kmajor ? K : M;
+    g.B = B;
+    g.b_kmajor = b_kmajor != 0;
+    g.ldb = b_kmajor ? K : N;
+    g.C = C;
+    g.ldc = N;
+    g.c = c_f32 ? spk::DType::kF32 : g.ab;
+    if (accumulate) {
+      if (!c_f32) throw std::invalid_argument("accumulate requires an fp32 C");
+      g.epi = spk::Epi::kAccumF32;
+    }
+    if (impl == spk::kGemmTcgen05 && !spk::gemm_tc_supported(g))
+      throw std::invalid_argument("tcgen05 GEMM does not support these operands");
+    spk::gemm(g, static_cast<cudaStream_t>(stream), impl);
+  });
+}
+
+int sp_attention_fwd(int32_t dtype, int32_t impl, const void* q, const void* kv, void* o, float* lse, int64_t n,
+                     int64_t q_off, int64_t kv_len, int32_t heads, int32_t head_dim, void* stream) {
+  return cuda_guard([&] {
+    spk::attn_fwd(dt(dtype), impl, q, kv, o, lse, n, q_off, kv_len, heads, head_dim, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int sp_attention_bwd(int32_t dtype, int32_t impl, const void* q, const void* kv, const void* o, const void* dout,
+                     const float* lse, void* dq, float* dkv_acc, int64_t n, int64_t q_off, int64_t kv_len, int32_t heads,
+                     int32_t head_dim, void* stream) {
+  return cuda_guard([&] {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    float* ws = nullptr;
+    const size_t floats = static_cast<size_t>(n) * heads + static_cast<size_t>(n) * heads * head_dim;
+    SPK_CUDA(cudaMallocAsync(&ws, floats * sizeof(float), s));
+    spk::attn_bwd(dt(dtype), impl, q, kv, o, dout, lse, ws, ws + static_cast<size_t>(n) * heads, dq, dkv_acc, n, q_off,
+                  kv_len, heads, head_dim, s);
+    SPK_CUDA(cudaFreeAsync(ws, s));
+  });
+}
+
+int sp_device_synchronize(int32_t cuda_device) {
+  return cuda_guard([&] {
+    SPK_CUDA(cudaSetDevice(cuda_device));
+    SPK_CUDA(cudaDeviceSynchronize());
+  });
+}
+
+int sp_cuda_device_count(int32_t* n) {
+  return cuda_guard([&] {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    *n = e == cudaSuccess ? c : 0;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,384 @@
+// HBM-bound kernels of the per-stage transformer: embedding, LayerNorm/RMSNorm
+// (fwd, recompute, bwd), GeLU/SwiGLU, RoPE, fused cross-entropy, AdamW, init.
+// One CTA per row for the row reductions (warp-shuffle + smem reduce), grid
+// sized to a multiple of the SM count for the streaming kernels.
+#include <cmath>
+
+#include "cuda/common.cuh"
+#include "cuda/ops.h"
+
+namespace spk {
+namespace {
+
+constexpr int kRowThreads = 256;
+
+int stream_grid(int64_t n, int threads) {
+  int64_t blocks = (n + threads - 1) / threads;
+  int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
+// ------------------------------------------------------------------ embedding
+template <typename T>
+__global__ void embed_fwd_k(const int32_t* __restrict__ tok, const float* __restrict__ E,
+                            const float* __restrict__ pos, int64_t pos0, T* __restrict__ x, int64_t n, int h) {
+  const int64_t total = n * h;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / h, c = i % h;
+    float v = E[(int64_t)tok[r] * h + c];
+    if (pos) v += pos[(pos0 + r) * h + c];
+    x[i] = from_f<T>(v);
+  }
+}
+
+template <typename T>
+__global__ void embed_bwd_k(const int32_t* __restrict__ tok, const T* __restrict__ dx, float* __restrict__ dE,
+                            float* __restrict__ dpos, int64_t pos0, int64_t n, int h) {
+  const int64_t total = n * h;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / h, c = i % h;
+    const float g = to_f(dx[i]);
+    atomicAdd(&dE[(int64_t)tok[r] * h + c], g);
+    if (dpos) dpos[(pos0 + r) * h + c] += g;  // positions are unique within a launch
+  }
+}
+
+// ------------------------------------------------------------------ norms
+template <typename T, bool RMS>
+__global__ void norm_fwd_k(const T* __restrict__ x, const float* __restrict__ g, T* __restrict__ y,
+                           float* __restrict__ mean_out, float* __restrict__ rstd_out, int h, float eps) {
+  __shared__ float scratch[32];
+  const int64_t row = blockIdx.x;
+  const T* xr = x + row * h;
+  float mean = 0.f;
+  if (!RMS) {
+    float s = 0.f;
+    for (int c = threadIdx.x; c < h; c += blockDim.x) s += to_f(xr[c]);
+    mean = block_sum(s, scratch) / h;
+  }
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) {
+    const float d = to_f(xr[c]) - mean;
+    ss += d * d;
+  }
+  const float rstd = rsqrtf(block_sum(ss, scratch) / h + eps);
+  T* yr = y + row * h;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) yr[c] = from_f<T>((to_f(xr[c]) - mean) * rstd * g[c]);
+  if (threadIdx.x == 0) {
+    if (!RMS) mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+template <typename T, bool RMS>
+__global__ void norm_apply_k(const T* __restrict__ x, const float* __restrict__ g, const float* __restrict__ mean,
+                             const float* __restrict__ rstd, T* __restrict__ y, int64_t n, int h) {
+  const int64_t total = n * h;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / h;
+    const int c = static_cast<int>(i % h);
+    const float mu = RMS ? 0.f : mean[r];
+    y[i] = from_f<T>((to_f(x[i]) - mu) * rstd[r] * g[c]);
+  }
+}
+
+// Rows are strided over the grid; each thread keeps partial dg for its
+// columns in registers-by-loop (accumulated in a per-block smem row) and the
+// block flushes once with atomics.
+template <typename T, bool RMS>
+__global__ void norm_bwd_k(const T* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ g,
+                           const float* __restrict__ mean, const float* __restrict__ rstd, const T* dres, T* dx,
+                           float* __restrict__ dg, int64_t n, int h) {
+  extern __shared__ float dg_part[];  // [h]
+  __shared__ float scratch[32];
+  for (int c = threadIdx.x; c < h; c += blockDim.x) dg_part[c] = 0.f;
+  for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
+    const T* xr = x + row * h;
+    const T* dyr = dy + row * h;
+    const float mu = RMS ? 0.f : mean[row];
+    const float rs = rstd[row];
+    float s1 = 0.f, s2 = 0.f;
+    for (int c = threadIdx.x; c < h; c += blockDim.x) {
+      const float xh = (to_f(xr[c]) - mu) * rs;
+      const float dxh = to_f(dyr[c]) * g[c];
+      s1 += dxh;
+      s2 += dxh * xh;
+      dg_part[c] += to_f(dyr[c]) * xh;
+    }
+    const float m1 = RMS ? 0.f : block_sum(s1, scratch) / h;
+    const float m2 = block_sum(s2, scratch) / h;
+    T* dxr = dx + row * h;
+    const T* drr = dres ? dres + row * h : nullptr;
+    for (int c = threadIdx.x; c < h; c += blockDim.x) {
+      const float xh = (to_f(xr[c]) - mu) * rs;
+      const float dxh = to_f(dyr[c]) * g[c];
+      float v = rs * (dxh - m1 - xh * m2);
+      if (drr) v += to_f(drr[c]);
+      dxr[c] = from_f<T>(v);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < h; c += blockDim.x) atomicAdd(&dg[c], dg_part[c]);
+}
+
+// ------------------------------------------------------------------ activations
+__device__ __forceinline__ float gelu_tanh(float u) {
+  const float c = 0.7978845608028654f;
+  return 0.5f * u * (1.f + tanhf(c * (u + 0.044715f * u * u * u)));
+}
+__device__ __forceinline__ float gelu_tanh_grad(float u) {
+  const float c = 0.7978845608028654f;
+  const float t = tanhf(c * (u + 0.044715f * u * u * u));
+  return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * u * u);
+}
+__device__ __forceinline__ float sigmoidf_(float u) { return 1.f / (1.f + expf(-u)); }
+
+template <typename T>
+__global__ void act_fwd_k(int family, const T* __restrict__ u, T* __restrict__ g, int64_t n, int F) {
+  const int64_t total = n * F;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    if (family == 0) {
+      g[i] = from_f<T>(gelu_tanh(to_f(u[i])));
+    } else {
+      const int64_t r = i / F, c = i % F;
+      const float a = to_f(u[r * 2 * F + c]), b = to_f(u[r * 2 * F + F + c]);
+      g[i] = from_f<T>(a * sigmoidf_(a) * b);
+    }
+  }
+}
+
+template <typename T>
+__global__ void act_bwd_k(int family, const T* __restrict__ u, const T* dg, T* du, int64_t n, int F) {
+  const int64_t total = n * F;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    if (family == 0) {
+      du[i] = from_f<T>(to_f(dg[i]) * gelu_tanh_grad(to_f(u[i])));
+    } else {
+      const int64_t r = i / F, c = i % F;
+      const float a = to_f(u[r * 2 * F + c]), b = to_f(u[r * 2 * F + F + c]);
+      const float d = to_f(dg[i]);  // dg may alias du's first half row-by-row: read before write
+      const float s = sigmoidf_(a);
+      const float da = d * b * s * (1.f + a * (1.f - s));
+      const float db = d * a * s;
+      du[r * 2 * F + c] = from_f<T>(da);
+      du[r * 2 * F + F + c] = from_f<T>(db);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ RoPE
+// Angles in double: positions reach 128K and fp32 sin/cos of large angles would
+// dominate the fp32 validation-mode error budget.
+template <typename T>
+__global__ void rope_k(T* x, int64_t ld, int64_t n, int H, int hd, int64_t pos0, float theta, bool inverse) {
+  const int half = hd / 2;
+  const int64_t total = n * H * half;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (H * half);
+    const int rem = static_cast<int>(i % (H * half));
+    const int head = rem / half, j = rem % half;
+    const double inv_freq = pow(static_cast<double>(theta), -2.0 * j / hd);
+    double sn, cs;
+    sincos(static_cast<double>(pos0 + r) * inv_freq, &sn, &cs);
+    T* p = x + r * ld + head * hd;
+    const double a = to_f(p[j]), b = to_f(p[j + half]);
+    const double s = inverse ? -sn : sn;
+    p[j] = from_f<T>(static_cast<float>(a * cs - b * s));
+    p[j + half] = from_f<T>(static_cast<float>(a * s + b * cs));
+  }
+}
+
+template <typename T>
+__global__ void assemble_dqkv_k(const T* __restrict__ dq, const float* __restrict__ dkv, T* __restrict__ out, int64_t n,
+                                int h) {
+  const int64_t total = n * 3 * h;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (3 * h);
+    const int c = static_cast<int>(i % (3 * h));
+    out[i] = c < h ? dq[r * h + c] : from_f<T>(dkv[r * 2 * h + (c - h)]);
+  }
+}
+
+// ------------------------------------------------------------------ cross-entropy
+template <typename T>
+__global__ void ce_k(T* logits, int64_t ld, const int32_t* __restrict__ labels, int V, float scale, double* loss) {
+  __shared__ float scratch[32];
+  const int64_t row = blockIdx.x;
+  T* lr = logits + row * ld;
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, to_f(lr[c]));
+  mx = block_max(mx, scratch);
+  float s = 0.f;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) s += expf(to_f(lr[c]) - mx);
+  s = block_sum(s, scratch);
+  const int lab = labels[row];
+  const float lab_logit = to_f(lr[lab]);
+  __syncthreads();
+  const float inv = 1.f / s;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    const float p = expf(to_f(lr[c]) - mx) * inv;
+    lr[c] = from_f<T>((p - (c == lab ? 1.f : 0.f)) * scale);
+  }
+  for (int64_t c = V + threadIdx.x; c < ld; c += blockDim.x) lr[c] = from_f<T>(0.f);  // padded vocab columns
+  if (threadIdx.x == 0) atomicAdd(loss, static_cast<double>(logf(s) + mx - lab_logit));
+}
+
+// ------------------------------------------------------------------ misc
+template <typename T>
+__global__ void cast_k(const float* __restrict__ src, T* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = from_f<T>(src[i]);
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_normal_k(float* p, int64_t n, uint64_t seed, float stddev) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = splitmix64(seed * 0x2545F4914F6CDD1DULL + static_cast<uint64_t>(i));
+    const double u1 = (static_cast<double>(r >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    const double u2 = static_cast<double>(splitmix64(r) >> 11) * (1.0 / 9007199254740992.0);
+    p[i] = static_cast<float>(stddev * sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
+  }
+}
+
+__global__ void fill_const_k(float* p, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+template <typename T>
+__global__ void adamw_k(float* p, const float* __restrict__ g, float* m, float* v, T* pc, int64_t n, float lr, float b1,
+                        float b2, float eps, float wd, float bc1, float bc2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    float pi = p[i];
+    pi -= lr * ((mi / bc1) / (sqrtf(vi / bc2) + eps) + wd * pi);
+    p[i] = pi;
+    if (pc) pc[i] = from_f<T>(pi);
+  }
+}
+
+}  // namespace
+
+#define SPK_DISPATCH(t, ...)                 \
+  if ((t) == DType::kF32) {                  \
+    using T = float;                         \
+    __VA_ARGS__;                             \
+  } else {                                   \
+    using T = __nv_bfloat16;                 \
+    __VA_ARGS__;                             \
+  }
+
+void embed_fwd(DType t, const int32_t* tok, const float* E, const float* pos, int64_t pos0, void* x, int64_t n, int h,
+               cudaStream_t s) {
+  SPK_DISPATCH(t, embed_fwd_k<T><<<stream_grid(n * h, 256), 256, 0, s>>>(tok, E, pos, pos0, (T*)x, n, h));
+  SPK_LAUNCH_CHECK();
+}
+
+void embed_bwd(DType t, const int32_t* tok, const void* dx, float* dE, float* dpos, int64_t pos0, int64_t n, int h,
+               cudaStream_t s) {
+  SPK_DISPATCH(t, embed_bwd_k<T><<<stream_grid(n * h, 256), 256, 0, s>>>(tok, (const T*)dx, dE, dpos, pos0, n, h));
+  SPK_LAUNCH_CHECK();
+}
+
+void norm_fwd(DType t, bool rms, const void* x, const float* g, void* y, float* mean, float* rstd, int64_t n, int h,
+              float eps, cudaStream_t s) {
+  if (n == 0) return;
+  SPK_DISPATCH(t, {
+    if (rms)
+      norm_fwd_k<T, true><<<n, kRowThreads, 0, s>>>((const T*)x, g, (T*)y, mean, rstd, h, eps);
+    else
+      norm_fwd_k<T, false><<<n, kRowThreads, 0, s>>>((const T*)x, g, (T*)y, mean, rstd, h, eps);
+  });
+  SPK_LAUNCH_CHECK();
+}
+
+void norm_apply(DType t, bool rms, const void* x, const float* g, const float* mean, const float* rstd, void* y,
+                int64_t n, int h, cudaStream_t s) {
+  SPK_DISPATCH(t, {
+    if (rms)
+      norm_apply_k<T, true><<<stream_grid(n * h, 256), 256, 0, s>>>((const T*)x, g, mean, rstd, (T*)y, n, h);
+    else
+      norm_apply_k<T, false><<<stream_grid(n * h, 256), 256, 0, s>>>((const T*)x, g, mean, rstd, (T*)y, n, h);
+  });
+  SPK_LAUNCH_CHECK();
+}
+
+void norm_bwd(DType t, bool rms, const void* dy, const void* x, const float* g, const float* mean, const float* rstd,
+              const void* dres, void* dx, float* dg, int64_t n, int h, cudaStream_t s) {
+  if (n == 0) return;
+  const int grid = static_cast<int>(n < 2 * num_sms() ? n : 2 * num_sms());
+  const size_t smem = sizeof(float) * h;
+  SPK_DISPATCH(t, {
+    if (rms) {
+      if (smem > 48 * 1024) cudaFuncSetAttribute(norm_bwd_k<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      norm_bwd_k<T, true><<<grid, kRowThreads, smem, s>>>((const T*)dy, (const T*)x, g, mean, rstd, (const T*)dres,
+                                                          (T*)dx, dg, n, h);
+    } else {
+      if (smem > 48 * 1024) cudaFuncSetAttribute(norm_bwd_k<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      norm_bwd_k<T, false><<<grid, kRowThreads, smem, s>>>((const T*)dy, (const T*)x, g, mean, rstd, (const T*)dres,
+                                                           (T*)dx, dg, n, h);
+    }
+  });
+  SPK_LAUNCH_CHECK();
+}
+
+void act_fwd(DType t, int family, const void* u, void* g, int64_t n, int F, cudaStream_t s) {
+  SPK_DISPATCH(t, act_fwd_k<T><<<stream_grid(n * F, 256), 256, 0, s>>>(family, (const T*)u, (T*)g, n, F));
+  SPK_LAUNCH_CHECK();
+}
+
+void act_bwd(DType t, int family, const void* u, const void* dg, void* du, int64_t n, int F, cudaStream_t s) {
+  SPK_DISPATCH(t, act_bwd_k<T><<<stream_grid(n * F, 256), 256, 0, s>>>(family, (const T*)u, (const T*)dg, (T*)du, n, F));
+  SPK_LAUNCH_CHECK();
+}
+
+void rope(DType t, void* x, int64_t ld, int64_t n, int H, int hd, int64_t pos0, float theta, bool inverse,
+          cudaStream_t s) {
+  SPK_DISPATCH(t, rope_k<T><<<stream_grid(n * H * hd / 2, 256), 256, 0, s>>>((T*)x, ld, n, H, hd, pos0, theta, inverse));
+  SPK_LAUNCH_CHECK();
+}
+
+void assemble_dqkv(DType t, const void* dq, const float* dkv, void* dqkv, int64_t n, int h, cudaStream_t s) {
+  SPK_DISPATCH(t, assemble_dqkv_k<T><<<stream_grid(n * 3 * h, 256), 256, 0, s>>>((const T*)dq, dkv, (T*)dqkv, n, h));
+  SPK_LAUNCH_CHECK();
+}
+
+void ce_fwd_bwd(DType t, void* logits, int64_t ld, const int32_t* labels, int64_t n, int V, float scale, double* loss,
+                cudaStream_t s) {
+  if (n == 0) return;
+  SPK_DISPATCH(t, ce_k<T><<<n, 512, 0, s>>>((T*)logits, ld, labels, V, scale, loss));
+  SPK_LAUNCH_CHECK();
+}
+
+void cast_from_f32(DType t, const float* src, void* dst, int64_t n, cudaStream_t s) {
+  SPK_DISPATCH(t, cast_k<T><<<stream_grid(n, 256), 256, 0, s>>>(src, (T*)dst, n));
+  SPK_LAUNCH_CHECK();
+}
+
+void fill_normal(float* p, int64_t n, uint64_t seed, float stddev, cudaStream_t s) {
+  fill_normal_k<<<stream_grid(n, 256), 256, 0, s>>>(p, n, seed, stddev);
+  SPK_LAUNCH_CHECK();
+}
+
+void fill_const(float* p, int64_t n, float v, cudaStream_t s) {
+  fill_const_k<<<stream_grid(n, 256), 256, 0, s>>>(p, n, v);
+  SPK_LAUNCH_CHECK();
+}
+
+void adamw(float* p, const float* g, float* m, float* v, void* pc, DType t, int64_t n, float lr, float b1, float b2,
+           float eps, float wd, int step, cudaStream_t s) {
+  const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
+  SPK_DISPATCH(t, adamw_k<T><<<stream_grid(n, 256), 256, 0, s>>>(p, g, m, v, (T*)pc, n, lr, b1, b2, eps, wd, bc1, bc2));
+  SPK_LAUNCH_CHECK();
+}
+
+}  // namespace spk

@@ -1,0 +1,186 @@
+// Seq1F1B execution engine: one object per device (GPU). It owns every
+// pipeline stage mapped to that device (stage -> device round-robin as
+// seqpipe::StageMap), executes the device's op order from seqpipe::generate()
+// with real sm_100a kernels, and reports SimReport-shaped measurements.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "cuda/common.cuh"
+#include "cuda/ops.h"
+#include "seqpipe/partition.hpp"
+#include "seqpipe/scenario.hpp"
+#include "seqpipe/schedule.hpp"
+#include "seqpipe_b200.h"
+
+namespace spe {
+
+using spk::DType;
+
+struct ModelCfg {
+  int family = SP_MODEL_GPT;
+  DType dt = DType::kBF16;
+  int V = 0, Vpad = 0, h = 0, L = 0, H = 0, hd = 0, F = 0, Fup = 0;
+  int64_t max_seq = 0;
+  uint64_t seed = 0;
+  float init_std = 0.02f, eps = 1e-5f, theta = 10000.f;
+  float lr = 0.f, b1 = 0.9f, b2 = 0.95f, adam_eps = 1e-8f, wd = 0.f;
+  int flags = 0;
+  bool rms() const { return family == SP_MODEL_LLAMA; }
+};
+
+struct Param {
+  std::string name;
+  int64_t off = 0, numel = 0;
+  int rows = 0, cols = 0;
+};
+
+// First-fit arena plan over a fixed alloc/free sequence.
+struct ArenaPlan {
+  int64_t size = 0;       // high-water mark of the address range
+  int64_t live_peak = 0;  // high-water mark of live bytes
+  std::map<int64_t, int64_t> free_;  // offset -> bytes
+  std::map<int64_t, int64_t> used_;
+  int64_t live = 0;
+  int64_t alloc(int64_t bytes);
+  void release(int64_t off);
+};
+
+class Stage {
+ public:
+  Stage(const ModelCfg& m, const seqpipe::ScenarioConfig& cfg, const std::vector<int64_t>& lengths, int stage,
+        int total_stages, cudaStream_t s);
+  ~Stage();
+
+  // Per-(micro-batch, segment) activation record inside the arena.
+  struct Seg {
+    int64_t n = 0, pos0 = 0;
+    std::vector<void*> x_in;  // L_s layer inputs [n,h]
+    void* x_out = nullptr;    // stage output [n,h]
+    void* dy_in = nullptr;    // gradient w.r.t. the stage output [n,h]
+    std::vector<void*> q, o, x_mid, u;
+    std::vector<float*> mean1, rstd1, mean2, rstd2, lse;
+  };
+
+  void plan_arena(const std::vector<seqpipe::Task>& order);
+  void bind_step();  // (re)bind Seg views to the arena for every (m,s) of this stage
+
+  void forward(int m, int s, const int32_t* tokens_dev, double* loss_acc, float loss_scale);
+  // dx_target: where the gradient w.r.t. this stage's input goes (another stage's dy_in or a send buffer).
+  void backward(int m, int s, void* dx_target, const int32_t* tokens_dev);
+
+  Seg& seg(int m, int s) { return segs_[(m - 1) * k_ + (s - 1)]; }
+  void* kv(int m, int layer) const;  // [T, 2h] slab of layer (local index)
+  float* dkv(int layer) const { return dkv_ + static_cast<size_t>(layer) * T_ * 2 * mc_.h; }
+
+  void zero_grads();
+  void sync_compute();  // recast the compute-dtype weight copy after a master write
+  void optimizer_step(int step);
+  void init_weights();
+  const std::vector<Param>& params() const { return params_; }
+  float* master() const { return master_; }
+  float* grads() const { return grad_; }
+  int64_t param_numel() const { return nparams_; }
+  double weight_bytes() const;
+  double arena_bytes() const { return static_cast<double>(arena_.size); }
+  double live_peak_bytes() const { return static_cast<double>(arena_.live_peak); }
+  double dkv_bytes() const { return static_cast<double>(L_s_) * T_ * 2 * mc_.h * 4; }
+  int stage() const { return stage_; }
+  bool first() const { return stage_ == 1; }
+  bool last() const { return stage_ == total_stages_; }
+
+  // Count of GEMM FLOPs + attention FLOPs (algorithmic) issued by this stage since the last reset.
+  double flops = 0;
+  int64_t launches = 0;
+
+ private:
+  struct LayerW {
+    int64_t norm1, wqkv, wo, norm2, w1, w2;
+  };
+  void* wc(int64_t off) const;  // compute-dtype weight pointer
+  float* wm(int64_t off) const { return master_ + off; }
+  float* wg(int64_t off) const { return grad_ + off; }
+  void gemm(const spk::GemmArgs& a, double flop);
+  void head_forward_backward(Seg& sg, int m, const int32_t* tokens_dev, double* loss_acc, float loss_scale);
+  int64_t add_param(const std::string& name, int rows, int cols);
+
+  ModelCfg mc_;
+  seqpipe::ScenarioConfig cfg_;
+  std::vector<int64_t> len_, prefix_;
+  int stage_, total_stages_, l0_, L_s_, k_, M_;
+  int64_t T_, nmax_;
+  cudaStream_t s_;
+  size_t esz_;
+
+  std::vector<Param> params_;
+  std::vector<LayerW> lw_;
+  int64_t embed_ = -1, pos_ = -1, fnorm_ = -1, lm_ = -1;
+  int64_t nparams_ = 0;
+  float *master_ = nullptr, *grad_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;
+  void* compute_ = nullptr;  // == master_ in fp32 mode
+
+  ArenaPlan arena_;
+  uint8_t* arena_ptr_ = nullptr;
+  std::vector<int64_t> seg_off_, kv_off_;
+  std::vector<Seg> segs_;
+  float* dkv_ = nullptr;
+
+  // workspace
+  void *w_a_ = nullptr, *w_big1_ = nullptr, *w_big2_ = nullptr, *w_t1_ = nullptr, *w_t2_ = nullptr, *w_t3_ = nullptr,
+       *w_dqkv_ = nullptr, *w_logits_ = nullptr;
+  float *w_delta_ = nullptr, *w_dq_ = nullptr, *w_fmean_ = nullptr, *w_frstd_ = nullptr;
+  int64_t logits_rows_ = 0;
+};
+
+class Engine {
+ public:
+  Engine(const seqpipe::ScenarioConfig& cfg, seqpipe::ScheduleKind kind, const std::vector<int64_t>& lengths,
+         const ModelCfg& m, int rank, int world, int cuda_device);
+  ~Engine();
+  void comm_init(const std::vector<std::string>& ids);
+  void step(const int32_t* tokens, bool on_device, sp_step_report* rep);
+  const std::vector<seqpipe::Task>& op_log() const { return op_log_; }
+  std::vector<std::vector<seqpipe::Task>> op_log_by_device() const;
+  const std::vector<double>& t_start() const { return t_start_; }
+  const std::vector<double>& t_end() const { return t_end_; }
+  Stage* stage_for_param(const std::string& name, Param* out);
+  std::vector<std::pair<Stage*, Param>> all_params();
+  int device() const { return dev_; }
+
+ private:
+  void exec_op(const seqpipe::Task& t, int order_index);
+  Stage* stage_obj(int stage) { return stages_.at(stage).get(); }
+
+  seqpipe::ScenarioConfig cfg_;
+  seqpipe::ScheduleKind kind_;
+  std::vector<int64_t> len_;
+  ModelCfg mc_;
+  int rank_, world_, dev_;
+  seqpipe::Schedule sched_;
+  std::vector<std::pair<int, int>> replay_;  // (device, position) execution order for this process
+  std::map<int, std::unique_ptr<Stage>> stages_;
+  cudaStream_t s_ = nullptr, s_send_ = nullptr, s_recv_ = nullptr;
+  int32_t* tokens_dev_ = nullptr;
+  int32_t* tokens_owned_ = nullptr;
+  double* loss_dev_ = nullptr;
+  int step_no_ = 0;
+  std::vector<seqpipe::Task> op_log_;
+  std::vector<cudaEvent_t> ev_start_, ev_end_;
+  cudaEvent_t ev_step0_ = nullptr, ev_step1_ = nullptr;
+  std::vector<double> t_start_, t_end_;
+  // NCCL: [0] activations on even edges, [1] odd edges, [2] grads even, [3] grads odd
+  ncclComm_t comms_[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool comm_ready_ = false;
+  std::vector<void*> send_ring_;
+  std::vector<cudaEvent_t> send_ring_ev_;
+  int send_ring_next_ = 0;
+  cudaEvent_t ev_tmp_ = nullptr;
+};
+
+}  // namespace spe

@@ -1,0 +1,160 @@
+"""Python handle over the sm_100a Seq1F1B execution engine (sp_engine_* C-ABI).
+
+`Engine(cfg, kind, partition, model)` runs every pipeline stage of `cfg` on one
+GPU when world_size == 1 (single-GPU validation layout) or one device's stages
+when launched one process per GPU (world_size == pipeline_size, NCCL P2P).
+There is no Python/CPU execution path: every call goes to libseqpipe_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from . import planner as pl
+
+GPT, LLAMA = 0, 1
+F32, BF16 = 0, 1
+FLAG_NO_TCGEN05, FLAG_NO_TC_ATTN, FLAG_TIMELINE = 1, 2, 4
+
+
+@dataclass
+class ModelConfig:
+    family: int = GPT
+    dtype: int = BF16
+    vocab: int = 50257
+    hidden: int = 256
+    layers: int = 8
+    heads: int = 4
+    head_dim: int = 64
+    ffn: int = 1024
+    max_seq: int = 2048
+    seed: int = 42
+    init_std: float = 0.02
+    norm_eps: float = 1e-5
+    rope_theta: float = 10000.0
+    lr: float = 0.0
+    beta1: float = 0.9
+    beta2: float = 0.95
+    adam_eps: float = 1e-8
+    weight_decay: float = 0.0
+    flags: int = 0
+
+    def to_c(self) -> _capi.Model:
+        m = _capi.Model()
+        for k, v in self.__dict__.items():
+            setattr(m, k, v)
+        return m
+
+    def param_count(self) -> int:
+        """Exact trainable parameter count of the instantiated model (untied head)."""
+        h, L, F, V = self.hidden, self.layers, self.ffn, self.vocab
+        fup = 2 * F if self.family == LLAMA else F
+        per_layer = 2 * h + 3 * h * h + h * h + fup * h + h * F
+        emb = V * h + (self.max_seq * h if self.family == GPT else 0)
+        return emb + L * per_layer + h + V * h
+
+
+def _check(code):
+    pl._check(code)
+
+
+class Engine:
+    def __init__(self, cfg: pl.ScenarioConfig, kind, partition: pl.SequencePartition, model: ModelConfig,
+                 rank: int = 0, world_size: int = 1, cuda_device: int = 0):
+        self.cfg, self.kind, self.partition, self.model = cfg, pl.SCHEDULE_KINDS[pl.kind_id(kind)], partition, model
+        self.rank, self.world_size = rank, world_size
+        self._h = C.c_void_p()
+        c = cfg.to_c()
+        lens = (C.c_int64 * len(partition.lengths))(*partition.lengths)
+        mc = model.to_c()
+        _check(_capi.lib().sp_engine_create(C.byref(c), pl.kind_id(kind), lens, C.byref(mc), rank, world_size,
+                                            cuda_device, C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            _capi.lib().sp_engine_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def comm_init(self, ids: list):
+        arr = (C.c_char_p * len(ids))(*ids)
+        _check(_capi.lib().sp_engine_comm_init(self._h, arr, len(ids)))
+
+    def step(self, tokens, on_device: bool = False) -> _capi.StepReport:
+        """One training step (all micro-batches, optimizer included). tokens: int32 [M, T+1]
+        host array, or a device pointer (int) when on_device."""
+        rep = _capi.StepReport()
+        if on_device:
+            ptr = C.c_void_p(int(tokens))
+        else:
+            tok = np.ascontiguousarray(tokens, dtype=np.int32)
+            assert tok.shape == (self.cfg.micro_batches, self.cfg.seq_len + 1), tok.shape
+            ptr = tok.ctypes.data_as(C.c_void_p)
+        _check(_capi.lib().sp_engine_step(self._h, ptr, 1 if on_device else 0, C.byref(rep)))
+        return rep
+
+    def op_log(self) -> pl.Schedule:
+        P = self.cfg.pipeline_size
+        counts = (C.c_int64 * P)()
+        _check(_capi.lib().sp_engine_op_log(self._h, None, counts))
+        ops = (_capi.Task * max(1, sum(counts)))()
+        _check(_capi.lib().sp_engine_op_log(self._h, ops, counts))
+        return pl.Schedule(self.cfg, self.kind, pl._unflatten(P, ops, counts))
+
+    def timeline(self):
+        n = C.c_int64(0)
+        _check(_capi.lib().sp_engine_timeline(self._h, None, None, C.byref(n)))
+        a = (C.c_double * max(1, n.value))()
+        b = (C.c_double * max(1, n.value))()
+        _check(_capi.lib().sp_engine_timeline(self._h, a, b, C.byref(n)))
+        return np.array(a[: n.value]), np.array(b[: n.value])
+
+    def params(self) -> dict:
+        """name -> (rows, cols) of every parameter held by this engine."""
+        n = C.c_int64()
+        _check(_capi.lib().sp_engine_param_count(self._h, C.byref(n)))
+        out = {}
+        for i in range(n.value):
+            name = C.create_string_buffer(128)
+            numel, r, c = C.c_int64(), C.c_int32(), C.c_int32()
+            _check(_capi.lib().sp_engine_param_info(self._h, i, name, 128, C.byref(numel), C.byref(r), C.byref(c)))
+            out[name.value.decode()] = (r.value, c.value)
+        return out
+
+    def _rows(self, name, rows):
+        return self.model.vocab if name == "lm_head" else rows
+
+    def read_param(self, name: str) -> np.ndarray:
+        r, c = self.params()[name]
+        r = self._rows(name, r)
+        out = np.empty((r, c), dtype=np.float32)
+        _check(_capi.lib().sp_engine_read_param(self._h, name.encode(), out.ctypes.data_as(C.POINTER(C.c_float)),
+                                                out.size))
+        return out
+
+    def read_grad(self, name: str) -> np.ndarray:
+        r, c = self.params()[name]
+        r = self._rows(name, r)
+        out = np.empty((r, c), dtype=np.float32)
+        _check(_capi.lib().sp_engine_read_grad(self._h, name.encode(), out.ctypes.data_as(C.POINTER(C.c_float)),
+                                               out.size))
+        return out
+
+    def write_param(self, name: str, value: np.ndarray):
+        v = np.ascontiguousarray(value, dtype=np.float32)
+        _check(_capi.lib().sp_engine_write_param(self._h, name.encode(), v.ctypes.data_as(C.POINTER(C.c_float)),
+                                                 v.size))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_capi.lib().sp_nccl_unique_id(buf, 128))
+    return buf.raw

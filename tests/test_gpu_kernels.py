@@ -1,0 +1,123 @@
+"""Kernel-level parity on the B200: tcgen05 GEMM (all operand majorness /
+epilogues) and prefix attention fwd/bwd against plain PyTorch fp32 references.
+Every call goes through the C-ABI (sp_gemm / sp_attention_*)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2406_03488_b200 import _capi  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+F32, BF16 = 0, 1
+
+
+def _gemm(impl, A, a_k, B, b_k, Cm, c_f32, acc, M, N, K):
+    code = _capi.lib().sp_gemm(BF16 if A.dtype == torch.bfloat16 else F32, impl, C.c_void_p(A.data_ptr()), a_k,
+                               C.c_void_p(B.data_ptr()), b_k, C.c_void_p(Cm.data_ptr()), c_f32, acc, M, N, K, None)
+    _capi.check(code)
+    torch.cuda.synchronize()
+
+
+def _rel(a, b):
+    a = a.double()
+    b = b.double()
+    return float((a - b).norm() / max(b.norm(), 1e-30))
+
+
+@pytest.mark.parametrize("a_k,b_k", [(1, 1), (1, 0), (0, 0), (0, 1)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (304, 520, 200), (1037, 768, 2560), (2048, 2560, 10170),
+                                   (10170, 7680, 2560)])
+def test_tcgen05_gemm_layouts(gpu, a_k, b_k, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
+    A = torch.randn((M, K) if a_k else (K, M), device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn((N, K) if b_k else (K, N), device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    lda, ldb = (K if a_k else M), (K if b_k else N)
+    if lda % 8 or ldb % 8:  # TMA needs 16-byte row strides: the C-ABI must refuse, not fall back
+        with pytest.raises(_capi.SeqpipeError):
+            _gemm(2, A, a_k, B, b_k, out, 1, 0, M, N, K)
+        return
+    Am = A.double() if a_k else A.double().t()
+    Bm = B.double() if b_k else B.double().t()
+    ref = Am @ Bm.t()
+    _gemm(2, A, a_k, B, b_k, out, 1, 0, M, N, K)
+    assert _rel(out, ref) < 1e-5, _rel(out, ref)
+    outb = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    _gemm(2, A, a_k, B, b_k, outb, 0, 0, M, N, K)
+    assert _rel(outb.float(), ref) < 8e-3
+    # fp32 accumulate epilogue (weight-gradient path)
+    base = torch.randn(M, N, device="cuda", generator=g)
+    acc = base.clone()
+    _gemm(2, A, a_k, B, b_k, acc, 1, 1, M, N, K)
+    assert _rel(acc, base + ref) < 1e-5
+
+
+def test_simt_gemm_fp32(gpu):
+    M, N, K = 333, 257, 129
+    A = torch.randn(K, M, device="cuda")
+    B = torch.randn(K, N, device="cuda")
+    out = torch.empty(M, N, device="cuda")
+    _gemm(1, A, 0, B, 0, out, 1, 0, M, N, K)
+    ref = A.double().t() @ B.double()
+    assert _rel(out, ref) < 1e-6
+
+
+def _attn_ref(q, kv, n, q_off, H, hd):
+    h = H * hd
+    L = q_off + n
+    qh = q.double().view(n, H, hd).transpose(0, 1)
+    kh = kv[:, :h].double().view(L, H, hd).transpose(0, 1)
+    vh = kv[:, h:].double().view(L, H, hd).transpose(0, 1)
+    S = qh @ kh.transpose(1, 2) / hd ** 0.5
+    mask = torch.arange(L, device="cuda")[None, :] > (q_off + torch.arange(n, device="cuda"))[:, None]
+    S = S.masked_fill(mask[None], float("-inf"))
+    lse = torch.logsumexp(S, dim=2)
+    P = torch.softmax(S, dim=2)
+    o = (P @ vh).transpose(0, 1).reshape(n, h)
+    return o, lse, P, qh, kh, vh
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("impl", [1, 0])
+@pytest.mark.parametrize("n,q_off,H,hd", [(77, 0, 2, 64), (130, 200, 4, 64), (96, 160, 3, 80), (200, 57, 2, 128)])
+def test_attention_fwd_bwd(gpu, dtype, impl, n, q_off, H, hd):
+    g = torch.Generator(device="cuda").manual_seed(n + q_off)
+    h = H * hd
+    L = q_off + n
+    q = torch.randn(n, h, device="cuda", generator=g).to(dtype)
+    kv = torch.randn(L, 2 * h, device="cuda", generator=g).to(dtype)
+    dout = torch.randn(n, h, device="cuda", generator=g).to(dtype)
+    o = torch.empty(n, h, device="cuda", dtype=dtype)
+    lse = torch.empty(H, n, device="cuda", dtype=torch.float32)
+    dt = F32 if dtype == torch.float32 else BF16
+    _capi.check(_capi.lib().sp_attention_fwd(dt, impl, C.c_void_p(q.data_ptr()), C.c_void_p(kv.data_ptr()),
+                                             C.c_void_p(o.data_ptr()), C.c_void_p(lse.data_ptr()), n, q_off, L, H, hd,
+                                             None))
+    torch.cuda.synchronize()
+    o_ref, lse_ref, P, qh, kh, vh = _attn_ref(q, kv, n, q_off, H, hd)
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    assert _rel(o.float(), o_ref) < tol
+    assert _rel(lse, lse_ref) < tol
+    # backward: dq and dK/dV accumulated (+=) into an fp32 buffer
+    dq = torch.empty(n, h, device="cuda", dtype=dtype)
+    base = torch.randn(L, 2 * h, device="cuda", generator=g)
+    dkv = base.clone()
+    _capi.check(_capi.lib().sp_attention_bwd(dt, impl, C.c_void_p(q.data_ptr()), C.c_void_p(kv.data_ptr()),
+                                             C.c_void_p(o.data_ptr()), C.c_void_p(dout.data_ptr()),
+                                             C.c_void_p(lse.data_ptr()), C.c_void_p(dq.data_ptr()),
+                                             C.c_void_p(dkv.data_ptr()), n, q_off, L, H, hd, None))
+    torch.cuda.synchronize()
+    doh = dout.double().view(n, H, hd).transpose(0, 1)
+    dP = doh @ vh.transpose(1, 2)
+    dv = P.transpose(1, 2) @ doh
+    dS = P * (dP - (dP * P).sum(-1, keepdim=True)) / hd ** 0.5
+    dq_ref = (dS @ kh).transpose(0, 1).reshape(n, h)
+    dk = (dS.transpose(1, 2) @ qh).transpose(0, 1).reshape(L, h)
+    dv = dv.transpose(0, 1).reshape(L, h)
+    tolb = 1e-5 if dtype == torch.float32 else 2e-2
+    assert _rel(dq.float(), dq_ref) < tolb
+    assert _rel(dkv[:, :h] - base[:, :h], dk) < tolb
+    assert _rel(dkv[:, h:] - base[:, h:], dv) < tolb
