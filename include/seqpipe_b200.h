@@ -228,7 +228,8 @@ typedef struct sp_model {
 enum {
   SP_FLAG_NO_TCGEN05 = 1,   /* bf16 mode: force the SIMT GEMM (debug / A-B testing)   */
   SP_FLAG_NO_TC_ATTN = 2,   /* bf16 mode: force the SIMT attention                    */
-  SP_FLAG_TIMELINE = 4      /* record per-op CUDA events for the measured report      */
+  SP_FLAG_TIMELINE = 4,     /* record per-op CUDA events for the measured report      */
+  SP_FLAG_KPROBE = 8        /* CUDA events around every GEMM / attention launch        */
 };
 
 typedef struct sp_engine sp_engine;
@@ -246,9 +247,15 @@ typedef struct sp_step_report {
   double weight_bytes;        /* params + grads + optimizer state                           */
   int64_t ops_executed;
   int64_t kernel_launches;
-  double dominant_kernel_ms;  /* summed duration of the dominant kernel (see engine)        */
+  double dominant_kernel_ms;  /* summed duration of the dominant kernel class (KPROBE)      */
   int64_t dominant_kernel_launches;
-  double dominant_kernel_flops;
+  double dominant_kernel_flops;  /* algorithmic FLOPs of those launches (all issued FLOPs when
+                                    KPROBE is off)                                          */
+  int32_t dominant_kernel_class; /* 0 tcgen05/SIMT GEMM, 1 attention fwd, 2 attention bwd   */
+  int32_t reserved0;
+  double class_ms[3];         /* per class: GEMM, attention fwd, attention bwd (KPROBE)      */
+  double class_flops[3];
+  int64_t class_launches[3];
 } sp_step_report;
 
 /* One engine = one device (all stages this device owns). world_size == pipeline_size for the
@@ -258,10 +265,17 @@ int sp_engine_create(const sp_scenario* cfg, int32_t schedule_kind, const int64_
                      const sp_model* model, int32_t rank, int32_t world_size, int32_t cuda_device,
                      sp_engine** out);
 int sp_engine_destroy(sp_engine* eng);
+/* Analytical activation footprint of one stage under a schedule (host-only replay of the
+ * engine's arena plan; no device memory): live high-water mark, arena size, and the fp32
+ * dK/dV accumulator. Used to report configurations that would not fit (e.g. 1F1B at 128K). */
+int sp_plan_memory(const sp_scenario* cfg, int32_t schedule_kind, const int64_t* lengths, const sp_model* model,
+                   int32_t stage, double* live_peak_bytes, double* arena_bytes, double* dkv_bytes);
 /* NCCL bootstrap: rank 0 calls sp_nccl_unique_id, the id bytes travel by any side channel,
  * every rank calls sp_engine_comm_init. */
 int sp_nccl_unique_id(uint8_t* out, size_t len);
 int sp_engine_comm_init(sp_engine* eng, const uint8_t* const* ids, int32_t n_ids);
+/* Replace the engine's SP_FLAG_* set (e.g. turn kernel probes on for a timed region). */
+int sp_engine_set_flags(sp_engine* eng, int32_t flags);
 /* tokens: micro_batches x (seq_len + 1) int32 (inputs are [:, :T], labels [:, 1:]).
  * tokens_on_device != 0 means `tokens` is a device pointer. */
 int sp_engine_step(sp_engine* eng, const int32_t* tokens, int32_t tokens_on_device,

@@ -78,6 +78,8 @@ class StepReport(C.Structure):
         ("peak_activation_bytes", C.c_double), ("arena_bytes", C.c_double), ("weight_bytes", C.c_double),
         ("ops_executed", C.c_int64), ("kernel_launches", C.c_int64), ("dominant_kernel_ms", C.c_double),
         ("dominant_kernel_launches", C.c_int64), ("dominant_kernel_flops", C.c_double),
+        ("dominant_kernel_class", C.c_int32), ("reserved0", C.c_int32),
+        ("class_ms", C.c_double * 3), ("class_flops", C.c_double * 3), ("class_launches", C.c_int64 * 3),
     ]
 
 
@@ -114,9 +116,12 @@ _SIGS = {
     "sp_engine_create": (C.c_int, [P(Scenario), C.c_int32, P(C.c_int64), P(Model), C.c_int32, C.c_int32,
                                    C.c_int32, P(C.c_void_p)]),
     "sp_engine_destroy": (C.c_int, [C.c_void_p]),
+    "sp_plan_memory": (C.c_int, [P(Scenario), C.c_int32, P(C.c_int64), P(Model), C.c_int32, P(C.c_double),
+                                 P(C.c_double), P(C.c_double)]),
     "sp_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_size_t]),
     "sp_engine_comm_init": (C.c_int, [C.c_void_p, P(C.c_char_p), C.c_int32]),
     "sp_engine_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, P(StepReport)]),
+    "sp_engine_set_flags": (C.c_int, [C.c_void_p, C.c_int32]),
     "sp_engine_op_log": (C.c_int, [C.c_void_p, P(Task), P(C.c_int64)]),
     "sp_engine_timeline": (C.c_int, [C.c_void_p, P(C.c_double), P(C.c_double), P(C.c_int64)]),
     "sp_engine_param_count": (C.c_int, [C.c_void_p, P(C.c_int64)]),
@@ -156,7 +161,7 @@ def lib():
         if not LIB_PATH.exists():
             raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2406_03488_b200.build` "
                                "(no CPU/Python fallback exists)")
-        _lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_GLOBAL if hasattr(os, "RTLD_GLOBAL") else 0)
+        _lib = C.CDLL(str(LIB_PATH))
         for name, (res, args) in _SIGS.items():
             fn = getattr(_lib, name, None)
             if fn is None:

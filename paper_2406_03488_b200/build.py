@@ -23,7 +23,23 @@ LIB = OUT / "libseqpipe_b200.so"
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA / "bin" / "nvcc")
 
-INCLUDES = [f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{CUDA / 'include'}"]
+def _nccl_dir() -> Path | None:
+    """NCCL shipped with this image's torch wheel (2.28.x). Linking against it (not the
+    older system libnccl) lets torch and this library share one libnccl.so.2 in a process."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        d = Path(list(spec.submodule_search_locations)[0])
+        if (d / "lib" / "libnccl.so.2").exists():
+            return d
+    return None
+
+
+NCCL = _nccl_dir()
+INCLUDES = [f"-I{ROOT / 'include'}", f"-I{CSRC}"] + ([f"-I{NCCL / 'include'}"] if NCCL else []) + \
+    [f"-I{CUDA / 'include'}"]
+NCCL_LINK = ([f"-L{NCCL / 'lib'}", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{NCCL / 'lib'}"] if NCCL
+             else ["-lnccl"])
 CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra", "-Wno-unused-parameter"]
 NVFLAGS = [
     "-std=c++20", "-O3", "-Xcompiler", "-fPIC", "-lineinfo",
@@ -81,7 +97,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
     cmd = [
         NVCC, "-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a",
         *map(str, objs), "-o", str(LIB),
-        f"-L{CUDA / 'lib64'}", "-lcudart", "-lnccl", "-ldl",
+        f"-L{CUDA / 'lib64'}", "-lcudart", *NCCL_LINK, "-ldl",
         "-Xlinker", "-rpath,$ORIGIN",
     ]
     if verbose:

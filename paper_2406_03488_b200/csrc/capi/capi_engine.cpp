@@ -88,6 +88,23 @@ int sp_engine_create(const sp_scenario* cfg, int32_t schedule_kind, const int64_
   });
 }
 
+int sp_plan_memory(const sp_scenario* cfg, int32_t schedule_kind, const int64_t* lengths, const sp_model* model,
+                   int32_t stage, double* live_peak_bytes, double* arena_bytes, double* dkv_bytes) {
+  return eguard([&] {
+    auto c = spc::from_c(cfg);
+    auto part = spc::partition_from_c(c, lengths, c.segments);
+    auto mc = model_from_c(model);
+    if (stage < 1 || stage > c.total_stages()) throw std::out_of_range("stage out of range");
+    if (mc.L % c.total_stages()) throw std::invalid_argument("model layers must divide evenly over the pipeline stages");
+    auto sch = seqpipe::generate(c, spc::kind_from_c(schedule_kind), part);
+    const int dev = (stage - 1) % c.pipeline_size;
+    auto plan = spe::plan_stage_memory(mc, c, part.lengths, sch.device_orders[static_cast<size_t>(dev)], stage);
+    if (live_peak_bytes) *live_peak_bytes = static_cast<double>(plan.live_peak);
+    if (arena_bytes) *arena_bytes = static_cast<double>(plan.size());
+    if (dkv_bytes) *dkv_bytes = static_cast<double>(mc.L / c.total_stages()) * c.seq_len * 2 * mc.h * 4;
+  });
+}
+
 int sp_engine_destroy(sp_engine* eng) {
   return eguard([&] { delete eng; });
 }
@@ -108,6 +125,10 @@ int sp_engine_comm_init(sp_engine* eng, const uint8_t* const* ids, int32_t n_ids
     for (int i = 0; i < n_ids; ++i) v.emplace_back(reinterpret_cast<const char*>(ids[i]), sizeof(ncclUniqueId));
     E(eng).comm_init(v);
   });
+}
+
+int sp_engine_set_flags(sp_engine* eng, int32_t flags) {
+  return eguard([&] { E(eng).set_flags(flags); });
 }
 
 int sp_engine_step(sp_engine* eng, const int32_t* tokens, int32_t tokens_on_device, sp_step_report* report) {

@@ -58,6 +58,7 @@ Engine::Engine(const seqpipe::ScenarioConfig& cfg, seqpipe::ScheduleKind kind, c
   for (auto& [v, st] : stages_) {
     const int d = (v - 1) % cfg_.pipeline_size + 1;
     st->plan_arena(sched_.device_orders[static_cast<size_t>(d - 1)]);
+    st->probe = &probe_;
   }
   // Execution order of this process: dependency-respecting interleaving of its device orders.
   if (world_ == 1) {
@@ -214,6 +215,8 @@ void Engine::step(const int32_t* tokens, bool on_device, sp_step_report* rep) {
     tokens_dev_ = tokens_owned_;
   }
   SPK_CUDA(cudaMemsetAsync(loss_dev_, 0, sizeof(double), s_));
+  probe_.enabled = (mc_.flags & SP_FLAG_KPROBE) != 0;
+  probe_.reset();
   int64_t launches0 = 0;
   for (auto& [v, st] : stages_) {
     st->zero_grads();
@@ -277,6 +280,22 @@ void Engine::step(const int32_t* tokens, bool on_device, sp_step_report* rep) {
     rep->ops_executed = static_cast<int64_t>(replay_.size());
     rep->kernel_launches = launches - launches0;
     rep->dominant_kernel_flops = flops;
+    if (probe_.enabled) {
+      double ms[KernelProbe::kNumClasses], fl[KernelProbe::kNumClasses];
+      int64_t cnt[KernelProbe::kNumClasses];
+      probe_.totals(ms, fl, cnt);
+      int dom = 0;
+      for (int c = 0; c < KernelProbe::kNumClasses; ++c) {
+        rep->class_ms[c] = ms[c];
+        rep->class_flops[c] = fl[c];
+        rep->class_launches[c] = cnt[c];
+        if (ms[c] > ms[dom]) dom = c;
+      }
+      rep->dominant_kernel_class = dom;
+      rep->dominant_kernel_ms = ms[dom];
+      rep->dominant_kernel_flops = fl[dom];
+      rep->dominant_kernel_launches = cnt[dom];
+    }
   }
 }
 

@@ -41,6 +41,31 @@ struct Param {
   int rows = 0, cols = 0;
 };
 
+// CUDA-event probes around every GEMM / attention launch (SP_FLAG_KPROBE):
+// per-class device time and algorithmic FLOPs for the live roofline.
+struct KernelProbe {
+  enum Class { kGemm = 0, kAttnFwd = 1, kAttnBwd = 2, kNumClasses = 3 };
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+    double flops;
+  };
+  std::vector<cudaEvent_t> pool;
+  std::vector<Rec> recs;
+  size_t next = 0;
+  bool enabled = false;
+  cudaEvent_t get();
+  void begin(int cls, cudaStream_t s, double flops);
+  void end(cudaStream_t s);
+  void reset() {
+    recs.clear();
+    next = 0;
+  }
+  // Sums per class after the stream has been synchronised.
+  void totals(double (&ms)[kNumClasses], double (&fl)[kNumClasses], int64_t (&n)[kNumClasses]);
+  ~KernelProbe();
+};
+
 // First-fit arena plan over a fixed alloc/free sequence.
 struct ArenaPlan {
   int64_t size = 0;       // high-water mark of the address range
@@ -51,6 +76,31 @@ struct ArenaPlan {
   int64_t alloc(int64_t bytes);
   void release(int64_t off);
 };
+
+// Two pools: fixed-size per-micro-batch KV-prefix slabs, and variable-size
+// per-(m,s) activation records. Separating them keeps the record pool from
+// fragmenting around the large slabs. Offsets of pool 1 are relative to the
+// end of pool 0 once finalised.
+struct DualArena {
+  ArenaPlan pool[2];
+  int64_t live = 0, live_peak = 0;
+  int64_t alloc(int p, int64_t bytes) {
+    const int64_t before = pool[p].live;
+    const int64_t off = pool[p].alloc(bytes);
+    live += pool[p].live - before;
+    live_peak = std::max(live_peak, live);
+    return off;
+  }
+  void release(int p, int64_t off) {
+    const int64_t before = pool[p].live;
+    pool[p].release(off);
+    live += pool[p].live - before;
+  }
+  int64_t size() const { return pool[0].size + pool[1].size; }
+};
+
+DualArena plan_stage_memory(const ModelCfg& mc, const seqpipe::ScenarioConfig& cfg, const std::vector<int64_t>& len,
+                            const std::vector<seqpipe::Task>& order, int stage);
 
 class Stage {
  public:
@@ -79,6 +129,7 @@ class Stage {
   void* kv(int m, int layer) const;  // [T, 2h] slab of layer (local index)
   float* dkv(int layer) const { return dkv_ + static_cast<size_t>(layer) * T_ * 2 * mc_.h; }
 
+  void set_flags(int f) { mc_.flags = f; }
   void zero_grads();
   void sync_compute();  // recast the compute-dtype weight copy after a master write
   void optimizer_step(int step);
@@ -88,7 +139,7 @@ class Stage {
   float* grads() const { return grad_; }
   int64_t param_numel() const { return nparams_; }
   double weight_bytes() const;
-  double arena_bytes() const { return static_cast<double>(arena_.size); }
+  double arena_bytes() const { return static_cast<double>(arena_.size()); }
   double live_peak_bytes() const { return static_cast<double>(arena_.live_peak); }
   double dkv_bytes() const { return static_cast<double>(L_s_) * T_ * 2 * mc_.h * 4; }
   int stage() const { return stage_; }
@@ -98,6 +149,7 @@ class Stage {
   // Count of GEMM FLOPs + attention FLOPs (algorithmic) issued by this stage since the last reset.
   double flops = 0;
   int64_t launches = 0;
+  KernelProbe* probe = nullptr;
 
  private:
   struct LayerW {
@@ -125,7 +177,7 @@ class Stage {
   float *master_ = nullptr, *grad_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;
   void* compute_ = nullptr;  // == master_ in fp32 mode
 
-  ArenaPlan arena_;
+  DualArena arena_;
   uint8_t* arena_ptr_ = nullptr;
   std::vector<int64_t> seg_off_, kv_off_;
   std::vector<Seg> segs_;
@@ -152,6 +204,10 @@ class Engine {
   Stage* stage_for_param(const std::string& name, Param* out);
   std::vector<std::pair<Stage*, Param>> all_params();
   int device() const { return dev_; }
+  void set_flags(int f) {
+    mc_.flags = f;
+    for (auto& kv : stages_) kv.second->set_flags(f);
+  }
 
  private:
   void exec_op(const seqpipe::Task& t, int order_index);
@@ -181,6 +237,7 @@ class Engine {
   std::vector<cudaEvent_t> send_ring_ev_;
   int send_ring_next_ = 0;
   cudaEvent_t ev_tmp_ = nullptr;
+  KernelProbe probe_;
 };
 
 }  // namespace spe

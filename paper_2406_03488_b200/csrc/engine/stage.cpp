@@ -233,24 +233,45 @@ static int64_t seg_bytes(const ModelCfg& mc, int L_s, int64_t n, size_t esz) {
   return b + 256LL * (8 * L_s + 4);        // per-field alignment slack
 }
 
-void Stage::plan_arena(const std::vector<seqpipe::Task>& order) {
-  arena_ = ArenaPlan{};
-  const int64_t kv_bytes = static_cast<int64_t>(L_s_) * T_ * 2 * mc_.h * esz_;
+// Host-only replay of the arena plan of one stage (no device memory): the
+// analytical activation footprint used to report OOM configurations.
+static DualArena replay_plan(const ModelCfg& mc, const seqpipe::ScenarioConfig& cfg, const std::vector<int64_t>& len,
+                             const std::vector<seqpipe::Task>& order, int stage, std::vector<int64_t>& seg,
+                             std::vector<int64_t>& kvo) {
+  const int L_s = mc.L / cfg.total_stages();
+  const size_t esz = spk::dtype_size(mc.dt);
+  const int64_t kv_bytes = static_cast<int64_t>(L_s) * cfg.seq_len * 2 * mc.h * esz;
+  DualArena a;
+  seg.assign(static_cast<size_t>(cfg.micro_batches) * cfg.segments, -1);
+  kvo.assign(static_cast<size_t>(cfg.micro_batches), -1);
   for (const seqpipe::Task& t : order) {
-    if (t.stage != stage_) continue;
-    const size_t idx = static_cast<size_t>(t.micro_batch - 1) * k_ + (t.segment - 1);
+    if (t.stage != stage) continue;
+    const size_t idx = static_cast<size_t>(t.micro_batch - 1) * cfg.segments + (t.segment - 1);
     if (t.kind == seqpipe::TaskKind::kForward) {
-      if (t.segment == 1) kv_off_[t.micro_batch - 1] = arena_.alloc(kv_bytes);
-      seg_off_[idx] = arena_.alloc(seg_bytes(mc_, L_s_, len_[t.segment - 1], esz_));
+      if (t.segment == 1) kvo[t.micro_batch - 1] = a.alloc(0, kv_bytes);
+      seg[idx] = a.alloc(1, seg_bytes(mc, L_s, len[t.segment - 1], esz));
     } else if (t.kind == seqpipe::TaskKind::kFusedBackward) {
-      arena_.release(seg_off_[idx]);
-      if (t.segment == 1) arena_.release(kv_off_[t.micro_batch - 1]);
+      a.release(1, seg[idx]);
+      if (t.segment == 1) a.release(0, kvo[t.micro_batch - 1]);
     } else {
       throw std::invalid_argument("engine executes F and B tasks (zero-bubble I/W split not supported yet)");
     }
   }
+  for (int64_t& o : seg)
+    if (o >= 0) o += a.pool[0].size;  // record pool sits after the slab pool
+  return a;
+}
+
+DualArena plan_stage_memory(const ModelCfg& mc, const seqpipe::ScenarioConfig& cfg, const std::vector<int64_t>& len,
+                            const std::vector<seqpipe::Task>& order, int stage) {
+  std::vector<int64_t> seg, kvo;
+  return replay_plan(mc, cfg, len, order, stage, seg, kvo);
+}
+
+void Stage::plan_arena(const std::vector<seqpipe::Task>& order) {
+  arena_ = replay_plan(mc_, cfg_, len_, order, stage_, seg_off_, kv_off_);
   if (arena_ptr_) cudaFree(arena_ptr_);
-  SPK_CUDA(cudaMalloc(&arena_ptr_, std::max<int64_t>(arena_.size, 256)));
+  SPK_CUDA(cudaMalloc(&arena_ptr_, std::max<int64_t>(arena_.size(), 256)));
   bind_step();
 }
 
@@ -307,9 +328,48 @@ void* Stage::kv(int m, int layer) const {
 void Stage::gemm(const GemmArgs& a, double flop) {
   int impl = spk::kGemmAuto;
   if (mc_.flags & SP_FLAG_NO_TCGEN05) impl = spk::kGemmSimt;
+  if (probe && probe->enabled) probe->begin(KernelProbe::kGemm, s_, flop);
   spk::gemm(a, s_, impl);
+  if (probe && probe->enabled) probe->end(s_);
   flops += flop;
   ++launches;
+}
+
+// ------------------------------------------------------------------ probes
+
+cudaEvent_t KernelProbe::get() {
+  if (next == pool.size()) {
+    cudaEvent_t e;
+    SPK_CUDA(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  return pool[next++];
+}
+
+void KernelProbe::begin(int cls, cudaStream_t s, double flops) {
+  Rec r{cls, get(), get(), flops};
+  SPK_CUDA(cudaEventRecord(r.a, s));
+  recs.push_back(r);
+}
+
+void KernelProbe::end(cudaStream_t s) { SPK_CUDA(cudaEventRecord(recs.back().b, s)); }
+
+void KernelProbe::totals(double (&ms)[kNumClasses], double (&fl)[kNumClasses], int64_t (&n)[kNumClasses]) {
+  for (int c = 0; c < kNumClasses; ++c) {
+    ms[c] = fl[c] = 0;
+    n[c] = 0;
+  }
+  for (const Rec& r : recs) {
+    float t = 0;
+    SPK_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.cls] += t;
+    fl[r.cls] += r.flops;
+    n[r.cls] += 1;
+  }
+}
+
+KernelProbe::~KernelProbe() {
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
 }
 
 namespace {
@@ -360,8 +420,11 @@ void Stage::forward(int m, int s, const int32_t* tokens, double* loss_acc, float
       spk::rope(dt, kv_rows, 2 * h, n, mc_.H, mc_.hd, pos0, mc_.theta, false, s_);
       launches += 2;
     }
+    const double attn_flops = 4.0 * h * (static_cast<double>(n) * pos0 + 0.5 * static_cast<double>(n) * n);
+    if (probe && probe->enabled) probe->begin(KernelProbe::kAttnFwd, s_, attn_flops);
     spk::attn_fwd(dt, attn_impl, sg.q[l], kv(m, l), sg.o[l], sg.lse[l], n, pos0, pos0 + n, mc_.H, mc_.hd, s_);
-    flops += 4.0 * h * (static_cast<double>(n) * pos0 + 0.5 * static_cast<double>(n) * n);
+    if (probe && probe->enabled) probe->end(s_);
+    flops += attn_flops;
     ++launches;
     g = G(dt, n, h, h, sg.o[l], h, true, wc(w.wo), h, true, sg.x_mid[l], h, dt);
     g.epi = Epi::kAddResid;
@@ -440,9 +503,13 @@ void Stage::backward(int m, int s, void* dx_target, const int32_t* tokens) {
     gemm(g, 2.0 * n * h * h);
     gemm(G(dt, n, h, h, w_t2_, h, true, wc(w.wo), h, false, w_t3_, h, dt), 2.0 * n * h * h);
     float* dkv_l = dkv(l);
+    // Algorithmic count: backward = 2x forward attention FLOPs (SURVEY §8d convention).
+    const double attn_flops = 2.0 * 4.0 * h * (static_cast<double>(n) * pos0 + 0.5 * static_cast<double>(n) * n);
+    if (probe && probe->enabled) probe->begin(KernelProbe::kAttnBwd, s_, attn_flops);
     spk::attn_bwd(dt, attn_impl, sg.q[l], kv(m, l), sg.o[l], w_t3_, sg.lse[l], w_delta_, w_dq_, w_t1_, dkv_l, n, pos0,
                   pos0 + n, mc_.H, mc_.hd, s_);
-    flops += 2.0 * 4.0 * h * (static_cast<double>(n) * pos0 + 0.5 * static_cast<double>(n) * n);
+    if (probe && probe->enabled) probe->end(s_);
+    flops += attn_flops;
     float* dkv_rows = dkv_l + pos0 * 2 * h;  // complete after this op (reverse causal order)
     if (mc_.family == SP_MODEL_LLAMA) {
       spk::rope(dt, w_t1_, h, n, mc_.H, mc_.hd, pos0, mc_.theta, true, s_);

@@ -17,7 +17,7 @@ from . import planner as pl
 
 GPT, LLAMA = 0, 1
 F32, BF16 = 0, 1
-FLAG_NO_TCGEN05, FLAG_NO_TC_ATTN, FLAG_TIMELINE = 1, 2, 4
+FLAG_NO_TCGEN05, FLAG_NO_TC_ATTN, FLAG_TIMELINE, FLAG_KPROBE = 1, 2, 4, 8
 
 
 @dataclass
@@ -83,6 +83,10 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+    def set_flags(self, flags: int):
+        self.model.flags = flags
+        _check(_capi.lib().sp_engine_set_flags(self._h, flags))
 
     def comm_init(self, ids: list):
         arr = (C.c_char_p * len(ids))(*ids)
@@ -152,6 +156,17 @@ class Engine:
         v = np.ascontiguousarray(value, dtype=np.float32)
         _check(_capi.lib().sp_engine_write_param(self._h, name.encode(), v.ctypes.data_as(C.POINTER(C.c_float)),
                                                  v.size))
+
+
+def plan_memory(cfg: pl.ScenarioConfig, kind, partition: pl.SequencePartition, model: ModelConfig, stage: int = 1):
+    """(live peak bytes, arena bytes, dKV accumulator bytes) of one stage, computed on the host."""
+    c = cfg.to_c()
+    lens = (C.c_int64 * len(partition.lengths))(*partition.lengths)
+    mc = model.to_c()
+    a, b, d = C.c_double(), C.c_double(), C.c_double()
+    _check(_capi.lib().sp_plan_memory(C.byref(c), pl.kind_id(kind), lens, C.byref(mc), stage, C.byref(a), C.byref(b),
+                                      C.byref(d)))
+    return a.value, b.value, d.value
 
 
 def nccl_unique_id() -> bytes:
