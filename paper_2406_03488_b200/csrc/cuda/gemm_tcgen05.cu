@@ -276,6 +276,8 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 }  // namespace
 
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() { return encode_fn(); }
+
 bool gemm_tc_supported(const GemmArgs& a) {
   if (a.ab != DType::kBF16) return false;
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return false;
