@@ -16,7 +16,12 @@ if [ ! -d "$REF/core/src" ]; then
   exit 0
 fi
 mkdir -p "$OUT/obj"
-CXX="${CXX:-g++}"
+# System g++ (same toolchain and libstdc++ as the engine build); ignores a CXX that may
+# point at a toolchain linking its own static libstdc++.
+CXX="${REF_CXX:-/usr/bin/g++}"
+# The reference defines the same seqpipe:: C++ symbols as the engine library; a
+# version script (ref_exports.map) keeps them local to this .so so a process
+# that loads both can never bind one library's calls to the other's code.
 FLAGS=(-std=c++20 -O2 -fPIC -I"$REF/core/include" -I"$NLOHMANN" -I"$HERE/../include")
 pids=()
 for src in "$REF"/core/src/*.cpp "$HERE/ref_shim.cpp"; do
@@ -27,5 +32,5 @@ for src in "$REF"/core/src/*.cpp "$HERE/ref_shim.cpp"; do
   fi
 done
 for p in "${pids[@]}"; do wait "$p"; done
-"$CXX" -shared -o "$OUT/libseqpipe_ref.so" "$OUT"/obj/*.o
+"$CXX" -shared -Wl,--version-script="$HERE/ref_exports.map" -o "$OUT/libseqpipe_ref.so" "$OUT"/obj/*.o
 echo "$OUT/libseqpipe_ref.so"

@@ -87,8 +87,7 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
   uint64_t* s_empty = bars + 9;  // [2]
   uint64_t* p_full = bars + 11;  // [2]
   uint64_t* p_empty = bars + 13; // [2]
-  uint64_t* o_full = bars + 15;  // [2]
-  uint64_t* o_empty = bars + 17; // [2]
+  uint64_t* o_done = bars + 15;  // one phase per PV MMA group
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -110,9 +109,8 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
       tc::mbar_init(&s_empty[i], 128);
       tc::mbar_init(&p_full[i], 128);
       tc::mbar_init(&p_empty[i], 1);
-      tc::mbar_init(&o_full[i], 1);
-      tc::mbar_init(&o_empty[i], 128);
     }
+    tc::mbar_init(o_done, 1);
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -166,7 +164,6 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
           const uint32_t ph = ((j - 1) >> 1) & 1;
           tc::mbar_wait(&p_full[b], ph);
           tc::mbar_wait(&v_full[b], ph);
-          tc::mbar_wait(&o_empty[b], ph ^ 1);
           tc::tc_fence_after();
           const uint32_t p_base = tc::smem_u32(sP + b * PBYTES);
           const uint32_t v_base = tc::smem_u32(sV + b * VBYTES);
@@ -174,49 +171,28 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
           for (int kk = 0; kk < BKV / 16; ++kk) {
             const uint64_t ad = tc::smem_desc(p_base + (kk >> 2) * CHUNK + (kk & 3) * 32, 16, 1024, tc::kSwizzle128B);
             const uint64_t bd = tc::smem_desc(v_base + kk * 2048, CHUNK, 1024, tc::kSwizzle128B);
-            tc::mma_bf16_ss(tmem + 256 + b * 128, ad, bd, idesc_o, kk > 0);
+            tc::mma_bf16_ss(tmem + 256, ad, bd, idesc_o, (j - 1) > 0 || kk > 0);  // O accumulates in TMEM
           }
-          tc::mma_commit(&o_full[b]);
+          tc::mma_commit(o_done);
           tc::mma_commit(&p_empty[b]);
           tc::mma_commit(&kv_empty[b]);
         }
       }
     }
   } else if (warp >= 4) {
+    // Softmax: S row in registers (one pass), P -> SMEM, O stays in TMEM. The
+    // running max used for exponentiation only moves when a block raises it by
+    // more than 2^8 (log2 domain); then the O row in TMEM is rescaled once
+    // PV_{j-1} has landed. Otherwise the softmax never waits for the PV MMAs.
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const int64_t row = q0 + r;
     const bool valid = row < p.n;
     const int64_t qpos = p.q_off + row;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
-    float acc[HD];
-#pragma unroll
-    for (int d = 0; d < HD; ++d) acc[d] = 0.f;
-
-    auto accumulate = [&](int jb, float alpha) {
-      const int b = jb & 1;
-      tc::mbar_wait(&o_full[b], (jb >> 1) & 1);
-      tc::tc_fence_after();
-      const uint32_t base = tmem + lane_base + 256 + b * 128;
-#pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t v[32];
-        tc::tmem_ld32(base + c * 32, v);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) acc[c * 32 + e] = acc[c * 32 + e] * alpha + __uint_as_float(v[e]);
-      }
-      if constexpr (HD % 32) {
-        uint32_t v[16];
-        tmem_ld16(base + (HD / 32) * 32, v);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 16; ++e) acc[(HD / 32) * 32 + e] = acc[(HD / 32) * 32 + e] * alpha + __uint_as_float(v[e]);
-      }
-      tc::tc_fence_before();
-      tc::mbar_arrive(&o_empty[b]);
-    };
+    const uint32_t obase = tmem + lane_base + 256;
+    constexpr float kRescale = 8.f;
+    float m = -INFINITY, l = 0.f;
 
     for (int j = 0; j < nblk; ++j) {
       const int b = j & 1;
@@ -226,59 +202,83 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
       tc::mbar_wait(&s_full[b], ph);
       tc::tc_fence_after();
       const uint32_t sbase = tmem + lane_base + b * 128;
+      uint32_t sv[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tc::tmem_ld32(sbase + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
+      tc::tmem_ld_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&s_empty[b]);  // S buffer free: the MMA warp may issue S_{j+2}
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tc::tmem_ld32(sbase + c * 32, v);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float s = (c * 32 + e <= lim) ? __uint_as_float(v[e]) * p.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, s);
-        }
+      for (int c = 0; c < 128; ++c) {
+        const float s = __uint_as_float(sv[c]) * p.scale_log2;
+        sv[c] = __float_as_uint(c <= lim ? s : -INFINITY);
+        mx = fmaxf(mx, __uint_as_float(sv[c]));
       }
-      const float m_new = fmaxf(m, mx);
-      const float m_use = m_new == -INFINITY ? 0.f : m_new;
-      const float alpha = m == -INFINITY ? 0.f : exp2f(m - m_new);
+      const bool need = (m == -INFINITY) ? (mx > -INFINITY || j == 0) : (mx > m + kRescale);
+      if (__any_sync(0xffffffffu, need)) {
+        const float m_new = need ? fmaxf(m, mx) : m;
+        const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
+        if (j > 0) {  // rescale the O row accumulated so far (PV_{j-1} must have landed)
+          tc::mbar_wait(o_done, (j - 1) & 1);
+          tc::tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < HD / 16; ++c) {
+            uint32_t v[16];
+            tmem_ld16(obase + c * 16, v);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+            tc::tmem_st16(obase + c * 16, v);
+          }
+          tc::tmem_st_wait();
+        }
+        l *= alpha;
+        m = m_new;
+      }
+      const float m_use = m == -INFINITY ? 0.f : m;
       tc::mbar_wait(&p_empty[b], ph ^ 1);
       uint8_t* ptile = sP + b * PBYTES;
       float rs = 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t v[32], w[16];
-        tc::tmem_ld32(sbase + c * 32, v);
-        tc::tmem_ld_wait();
+        uint32_t w[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const float p0 = (c * 32 + e <= lim) ? exp2f(__uint_as_float(v[e]) * p.scale_log2 - m_use) : 0.f;
-          const float p1 = (c * 32 + e + 1 <= lim) ? exp2f(__uint_as_float(v[e + 1]) * p.scale_log2 - m_use) : 0.f;
+          const float p0 = exp2f(__uint_as_float(sv[c * 32 + e]) - m_use);
+          const float p1 = exp2f(__uint_as_float(sv[c * 32 + e + 1]) - m_use);
           rs += p0 + p1;
           w[e / 2] = pack_bf16(p0, p1);
         }
         st_tile_row32(ptile, r, c, w);
       }
+      l += rs;
       tc::tc_fence_before();
-      tc::mbar_arrive(&s_empty[b]);
       fence_async_smem();
       tc::mbar_arrive(&p_full[b]);
-      l = l * alpha + rs;
-      m = m_new;
-      if (j >= 1) accumulate(j - 1, alpha_prev);
-      alpha_prev = alpha;
     }
-    if (nblk >= 1) accumulate(nblk - 1, alpha_prev);
-    if (valid) {
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* orow = p.o + row * p.h + head * HD;
+    tc::mbar_wait(o_done, (nblk - 1) & 1);  // last PV landed
+    tc::tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow = p.o + (valid ? row : 0) * p.h + head * HD;
 #pragma unroll
-      for (int d = 0; d < HD; d += 8) {
-        uint4 u = make_uint4(pack_bf16(acc[d] * inv, acc[d + 1] * inv), pack_bf16(acc[d + 2] * inv, acc[d + 3] * inv),
-                             pack_bf16(acc[d + 4] * inv, acc[d + 5] * inv), pack_bf16(acc[d + 6] * inv, acc[d + 7] * inv));
-        *reinterpret_cast<uint4*>(orow + d) = u;
-      }
-      p.lse[static_cast<int64_t>(head) * p.n + row] = (m + log2f(l)) * 0.69314718055994531f;
+    for (int c = 0; c < HD / 16; ++c) {
+      uint32_t v[16];
+      tmem_ld16(obase + c * 16, v);  // warp-collective
+      tc::tmem_ld_wait();
+      if (!valid) continue;
+      uint4 u0 = make_uint4(pack_bf16(__uint_as_float(v[0]) * inv, __uint_as_float(v[1]) * inv),
+                            pack_bf16(__uint_as_float(v[2]) * inv, __uint_as_float(v[3]) * inv),
+                            pack_bf16(__uint_as_float(v[4]) * inv, __uint_as_float(v[5]) * inv),
+                            pack_bf16(__uint_as_float(v[6]) * inv, __uint_as_float(v[7]) * inv));
+      uint4 u1 = make_uint4(pack_bf16(__uint_as_float(v[8]) * inv, __uint_as_float(v[9]) * inv),
+                            pack_bf16(__uint_as_float(v[10]) * inv, __uint_as_float(v[11]) * inv),
+                            pack_bf16(__uint_as_float(v[12]) * inv, __uint_as_float(v[13]) * inv),
+                            pack_bf16(__uint_as_float(v[14]) * inv, __uint_as_float(v[15]) * inv));
+      *reinterpret_cast<uint4*>(orow + c * 16) = u0;
+      *reinterpret_cast<uint4*>(orow + c * 16 + 8) = u1;
     }
+    if (valid) p.lse[static_cast<int64_t>(head) * p.n + row] = (m + log2f(l)) * 0.69314718055994531f;
   }
   tc::tc_fence_before();
   __syncthreads();
