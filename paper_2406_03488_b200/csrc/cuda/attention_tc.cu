@@ -63,6 +63,13 @@ __device__ __forceinline__ void st_tile_row32(uint8_t* tile, int r, int c32, con
   }
 }
 
+// One MUFU.EX2 (exp2f() adds range-reduction FMUL/FSETP/FSEL around it).
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -208,13 +215,20 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
       tc::tmem_ld_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&s_empty[b]);  // S buffer free: the MMA warp may issue S_{j+2}
+      // Raw scores stay unscaled (scale > 0 commutes with max); masking only on
+      // blocks that touch the causal diagonal or the prefix end.
       float mx = -INFINITY;
+      if (__all_sync(0xffffffffu, lim >= BKV - 1)) {
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        const float s = __uint_as_float(sv[c]) * p.scale_log2;
-        sv[c] = __float_as_uint(c <= lim ? s : -INFINITY);
-        mx = fmaxf(mx, __uint_as_float(sv[c]));
+        for (int c = 0; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(sv[c]));
+      } else {
+#pragma unroll
+        for (int c = 0; c < 128; ++c) {
+          if (c > lim) sv[c] = __float_as_uint(-INFINITY);
+          mx = fmaxf(mx, __uint_as_float(sv[c]));
+        }
       }
+      mx *= p.scale_log2;
       const bool need = (m == -INFINITY) ? (mx > -INFINITY || j == 0) : (mx > m + kRescale);
       if (__any_sync(0xffffffffu, need)) {
         const float m_new = need ? fmaxf(m, mx) : m;
@@ -236,22 +250,24 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
         l *= alpha;
         m = m_new;
       }
-      const float m_use = m == -INFINITY ? 0.f : m;
+      const float neg_m = m == -INFINITY ? 0.f : -m;
       tc::mbar_wait(&p_empty[b], ph ^ 1);
       uint8_t* ptile = sP + b * PBYTES;
-      float rs = 0.f;
+      float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t w[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const float p0 = exp2f(__uint_as_float(sv[c * 32 + e]) - m_use);
-          const float p1 = exp2f(__uint_as_float(sv[c * 32 + e + 1]) - m_use);
-          rs += p0 + p1;
+          const float p0 = ex2(fmaf(__uint_as_float(sv[c * 32 + e]), p.scale_log2, neg_m));
+          const float p1 = ex2(fmaf(__uint_as_float(sv[c * 32 + e + 1]), p.scale_log2, neg_m));
+          rs0 += p0;
+          rs1 += p1;
           w[e / 2] = pack_bf16(p0, p1);
         }
         st_tile_row32(ptile, r, c, w);
       }
+      const float rs = rs0 + rs1;
       l += rs;
       tc::tc_fence_before();
       fence_async_smem();
@@ -320,25 +336,26 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
   constexpr int Q_T = NC * CHUNK / 2;    // [64 rows x hd] tile (chunks of 8 KB)
   constexpr int QCH = CHUNK / 2;
   constexpr int PT = CHUNK;              // [128 keys x 64 queries] bf16 tile
+  constexpr int QST = NC == 1 ? 4 : 3;   // Q / dO / (LSE, delta) ring depth
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = sm;
   uint8_t* sV = sK + KV_T;
-  uint8_t* sQ = sV + KV_T;        // [2]
-  uint8_t* sdO = sQ + 2 * Q_T;    // [2]
-  uint8_t* sPt = sdO + 2 * Q_T;   // [2]
-  uint8_t* sdSt = sPt + 2 * PT;   // [2]
-  float* sLD = reinterpret_cast<float*>(sdSt + 2 * PT);  // [2][2][64]: lse*log2e, delta
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + 256);
+  uint8_t* sQ = sV + KV_T;          // [QST]
+  uint8_t* sdO = sQ + QST * Q_T;    // [QST]
+  uint8_t* sPt = sdO + QST * Q_T;   // [2]
+  uint8_t* sdSt = sPt + 2 * PT;     // [2]
+  float* sLD = reinterpret_cast<float*>(sdSt + 2 * PT);  // [QST][128]: lse*log2e (64), delta (64)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + QST * 128);
   uint64_t* kv_full = bars;
-  uint64_t* q_full = bars + 1;   // [2]
-  uint64_t* q_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;   // [2]
-  uint64_t* s_empty = bars + 7;  // [2]
-  uint64_t* p_full = bars + 9;   // [2]
-  uint64_t* p_empty = bars + 11; // [2]
-  uint64_t* done = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* s_full = bars + 1;   // [2]
+  uint64_t* s_empty = bars + 3;  // [2]
+  uint64_t* p_full = bars + 5;   // [2]
+  uint64_t* p_empty = bars + 7;  // [2]
+  uint64_t* done = bars + 9;
+  uint64_t* q_full = bars + 10;          // [QST]
+  uint64_t* q_empty = q_full + QST;      // [QST]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + QST);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int num_kb = static_cast<int>((p.kv_len + 127) / 128);
@@ -354,12 +371,14 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
     tc::mbar_init(kv_full, 1);
     tc::mbar_init(done, 1);
     for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&q_full[i], 1);
-      tc::mbar_init(&q_empty[i], 1);
       tc::mbar_init(&s_full[i], 1);
       tc::mbar_init(&s_empty[i], 128);
       tc::mbar_init(&p_full[i], 128);
       tc::mbar_init(&p_empty[i], 1);
+    }
+    for (int i = 0; i < QST; ++i) {
+      tc::mbar_init(&q_full[i], 1);
+      tc::mbar_init(&q_empty[i], 1);
     }
     tc::fence_mbar_init();
   }
@@ -371,6 +390,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
   // TMEM: S^T[2] at 0/64, dP^T[2] at 128/192, dV at 256, dK at 384.
 
   if (warp == 0) {
+    // Producer warp: K/V once; per query block the Q / dO tiles (TMA) and the
+    // block's LSE / delta vectors (all 32 lanes), QST stages ahead of the consumers.
     if (lane == 0) {
       tc::tma_prefetch(&p.tq);
       tc::tma_prefetch(&p.tdo);
@@ -380,16 +401,31 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
         tc::tma_load_2d(sK + c * CHUNK, &p.tkv, kv_full, head * HD + 64 * c, static_cast<int>(j0));
         tc::tma_load_2d(sV + c * CHUNK, &p.tkv, kv_full, p.h + head * HD + 64 * c, static_cast<int>(j0));
       }
-      for (int it = 0; it < niter; ++it) {
-        const int b = it & 1;
-        const int i0 = static_cast<int>(ib0) + it * 64;
-        tc::mbar_wait(&q_empty[b], ((it >> 1) & 1) ^ 1);
-        tc::mbar_expect_tx(&q_full[b], 2 * Q_T);
+    }
+    for (int it = 0; it < niter; ++it) {
+      const int st = it % QST;
+      const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
+      tc::mbar_wait(&q_empty[st], ((it / QST) & 1) ^ 1);
+      float* ld = sLD + st * 128;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = lane + 32 * u;
+        const int64_t qi = i0 + (idx & 63);
+        float v = 0.f;
+        if (qi < p.n)
+          v = idx < 64 ? p.lse[static_cast<int64_t>(head) * p.n + qi] * 1.4426950408889634f
+                       : p.delta[static_cast<int64_t>(head) * p.n + qi];
+        ld[idx] = v;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        tc::mbar_expect_tx(&q_full[st], 2 * Q_T);  // also publishes the LSE / delta stores
         for (int c = 0; c < NC; ++c) {
-          tc::tma_load_2d(sQ + b * Q_T + c * QCH, &p.tq, &q_full[b], head * HD + 64 * c, i0);
-          tc::tma_load_2d(sdO + b * Q_T + c * QCH, &p.tdo, &q_full[b], head * HD + 64 * c, i0);
+          tc::tma_load_2d(sQ + st * Q_T + c * QCH, &p.tq, &q_full[st], head * HD + 64 * c, static_cast<int>(i0));
+          tc::tma_load_2d(sdO + st * Q_T + c * QCH, &p.tdo, &q_full[st], head * HD + 64 * c, static_cast<int>(i0));
         }
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -399,12 +435,12 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
       const uint32_t k_base = tc::smem_u32(sK), v_base = tc::smem_u32(sV);
       for (int it = 0; it <= niter; ++it) {
         if (it < niter) {
-          const int b = it & 1;
+          const int b = it & 1, st = it % QST;
           const uint32_t ph = (it >> 1) & 1;
-          tc::mbar_wait(&q_full[b], ph);
+          tc::mbar_wait(&q_full[st], (it / QST) & 1);
           tc::mbar_wait(&s_empty[b], ph ^ 1);
           tc::tc_fence_after();
-          const uint32_t q_base = tc::smem_u32(sQ + b * Q_T), do_base = tc::smem_u32(sdO + b * Q_T);
+          const uint32_t q_base = tc::smem_u32(sQ + st * Q_T), do_base = tc::smem_u32(sdO + st * Q_T);
 #pragma unroll
           for (int kk = 0; kk < HD / 16; ++kk) {
             const uint32_t off_kv = (kk >> 2) * CHUNK + (kk & 3) * 32;
@@ -417,12 +453,12 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
           tc::mma_commit(&s_full[b]);
         }
         if (it >= 1) {
-          const int b = (it - 1) & 1;
+          const int b = (it - 1) & 1, st = (it - 1) % QST;
           const uint32_t ph = ((it - 1) >> 1) & 1;
           tc::mbar_wait(&p_full[b], ph);
           tc::tc_fence_after();
           const uint32_t pt = tc::smem_u32(sPt + b * PT), dst = tc::smem_u32(sdSt + b * PT);
-          const uint32_t q_base = tc::smem_u32(sQ + b * Q_T), do_base = tc::smem_u32(sdO + b * Q_T);
+          const uint32_t q_base = tc::smem_u32(sQ + st * Q_T), do_base = tc::smem_u32(sdO + st * Q_T);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries
             const bool acc = (it - 1) > 0 || kk > 0;
@@ -432,7 +468,7 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
                             tc::smem_desc(q_base + kk * 2048, QCH, 1024, tc::kSwizzle128B), idesc_g, acc);
           }
           tc::mma_commit(&p_empty[b]);
-          tc::mma_commit(&q_empty[b]);
+          tc::mma_commit(&q_empty[st]);
         }
       }
       tc::mma_commit(done);
@@ -442,21 +478,12 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
     const int r = quarter * 32 + lane;  // key row
     const int64_t kpos = j0 + r;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    const int t = threadIdx.x - 128;
     for (int it = 0; it < niter; ++it) {
-      const int b = it & 1;
+      const int b = it & 1, st = it % QST;
       const uint32_t ph = (it >> 1) & 1;
       const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
-      float* ld = sLD + b * 128;
-      {  // stage this query block's LSE (log2 units) and delta
-        const int64_t qi = i0 + (t & 63);
-        const bool ok = qi < p.n;
-        if (t < 64)
-          ld[t] = ok ? p.lse[static_cast<int64_t>(head) * p.n + qi] * 1.4426950408889634f : 0.f;
-        else
-          ld[t] = ok ? p.delta[static_cast<int64_t>(head) * p.n + qi] : 0.f;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-      }
+      const float* ld = sLD + st * 128;
+      tc::mbar_wait(&q_full[st], (it / QST) & 1);  // LSE / delta of this block are in SMEM
       // visible query columns c: q_off + i0 + c >= kpos and i0 + c < n
       int64_t cmin = kpos - p.q_off - i0;
       const int c_lo = cmin < 0 ? 0 : (cmin > 64 ? 64 : static_cast<int>(cmin));
@@ -474,22 +501,29 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
       tc::mbar_wait(&p_empty[b], ph ^ 1);
       uint8_t* ptile = sPt + b * PT;
       uint8_t* dstile = sdSt + b * PT;
+      const bool full_blk = __all_sync(0xffffffffu, c_lo == 0 && c_hi == 64);
 #pragma unroll
       for (int c32 = 0; c32 < 2; ++c32) {
         uint32_t wp[16], wd[16];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float pv[2], dv[2];
+        for (int e = 0; e < 32; e += 4) {
+          const int c0 = c32 * 32 + e;
+          const float4 l4 = *reinterpret_cast<const float4*>(ld + c0);       // LSE (log2) of 4 queries
+          const float4 d4 = *reinterpret_cast<const float4*>(ld + 64 + c0);  // delta of 4 queries
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
+          float pv[4], dv[4];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int c = c32 * 32 + e + u;
-            const bool vis = c >= c_lo && c < c_hi;
-            const float pr = vis ? exp2f(__uint_as_float(sv[c]) * p.scale_log2 - ld[c]) : 0.f;
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + u;
+            float pr = ex2(fmaf(__uint_as_float(sv[c]), p.scale_log2, -lv[u]));
+            if (!full_blk && (c < c_lo || c >= c_hi)) pr = 0.f;
             pv[u] = pr;
-            dv[u] = pr * (__uint_as_float(dpv[c]) - ld[64 + c]);
+            dv[u] = pr * (__uint_as_float(dpv[c]) - dl[u]);
           }
           wp[e / 2] = pack_bf16(pv[0], pv[1]);
+          wp[e / 2 + 1] = pack_bf16(pv[2], pv[3]);
           wd[e / 2] = pack_bf16(dv[0], dv[1]);
+          wd[e / 2 + 1] = pack_bf16(dv[2], dv[3]);
         }
         st_tile_row32(ptile, r, c32, wp);
         st_tile_row32(dstile, r, c32, wd);
@@ -543,21 +577,22 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ 
   constexpr int DS_T = CHUNK;            // [128 q x 64 keys]
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int KST = 4;  // K/V ring depth
   uint8_t* sQ = sm;
   uint8_t* sdO = sQ + Q_T;
-  uint8_t* sK = sdO + Q_T;    // [2]
-  uint8_t* sV = sK + 2 * K_T; // [2]
-  uint8_t* sdS = sV + 2 * K_T; // [2]
+  uint8_t* sK = sdO + Q_T;       // [KST]
+  uint8_t* sV = sK + KST * K_T;  // [KST]
+  uint8_t* sdS = sV + KST * K_T; // [2]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + 2 * DS_T);
   uint64_t* qo_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_empty = bars + 7;   // [2]
-  uint64_t* ds_full = bars + 9;   // [2]
-  uint64_t* ds_empty = bars + 11; // [2]
-  uint64_t* done = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* s_full = bars + 1;    // [2]
+  uint64_t* s_empty = bars + 3;   // [2]
+  uint64_t* ds_full = bars + 5;   // [2]
+  uint64_t* ds_empty = bars + 7;  // [2]
+  uint64_t* done = bars + 9;
+  uint64_t* kv_full = bars + 10;          // [KST]
+  uint64_t* kv_empty = kv_full + KST;     // [KST]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + KST);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int num_qb = static_cast<int>((p.n + 127) / 128);
@@ -572,12 +607,14 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ 
     tc::mbar_init(qo_full, 1);
     tc::mbar_init(done, 1);
     for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&kv_full[i], 1);
-      tc::mbar_init(&kv_empty[i], 1);
       tc::mbar_init(&s_full[i], 1);
       tc::mbar_init(&s_empty[i], 128);
       tc::mbar_init(&ds_full[i], 128);
       tc::mbar_init(&ds_empty[i], 1);
+    }
+    for (int i = 0; i < KST; ++i) {
+      tc::mbar_init(&kv_full[i], 1);
+      tc::mbar_init(&kv_empty[i], 1);
     }
     tc::fence_mbar_init();
   }
@@ -599,12 +636,12 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ 
         tc::tma_load_2d(sdO + c * CHUNK, &p.tdo, qo_full, head * HD + 64 * c, static_cast<int>(q0));
       }
       for (int j = 0; j < nblk; ++j) {
-        const int b = j & 1;
-        tc::mbar_wait(&kv_empty[b], ((j >> 1) & 1) ^ 1);
-        tc::mbar_expect_tx(&kv_full[b], 2 * K_T);
+        const int st = j % KST;
+        tc::mbar_wait(&kv_empty[st], ((j / KST) & 1) ^ 1);
+        tc::mbar_expect_tx(&kv_full[st], 2 * K_T);
         for (int c = 0; c < NC; ++c) {
-          tc::tma_load_2d(sK + b * K_T + c * KCH, &p.tkv, &kv_full[b], head * HD + 64 * c, j * 64);
-          tc::tma_load_2d(sV + b * K_T + c * KCH, &p.tkv, &kv_full[b], p.h + head * HD + 64 * c, j * 64);
+          tc::tma_load_2d(sK + st * K_T + c * KCH, &p.tkv, &kv_full[st], head * HD + 64 * c, j * 64);
+          tc::tma_load_2d(sV + st * K_T + c * KCH, &p.tkv, &kv_full[st], p.h + head * HD + 64 * c, j * 64);
         }
       }
     }
@@ -616,12 +653,12 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ 
       const uint32_t q_base = tc::smem_u32(sQ), do_base = tc::smem_u32(sdO);
       for (int j = 0; j <= nblk; ++j) {
         if (j < nblk) {
-          const int b = j & 1;
+          const int b = j & 1, st = j % KST;
           const uint32_t ph = (j >> 1) & 1;
-          tc::mbar_wait(&kv_full[b], ph);
+          tc::mbar_wait(&kv_full[st], (j / KST) & 1);
           tc::mbar_wait(&s_empty[b], ph ^ 1);
           tc::tc_fence_after();
-          const uint32_t k_base = tc::smem_u32(sK + b * K_T), v_base = tc::smem_u32(sV + b * K_T);
+          const uint32_t k_base = tc::smem_u32(sK + st * K_T), v_base = tc::smem_u32(sV + st * K_T);
 #pragma unroll
           for (int kk = 0; kk < HD / 16; ++kk) {
             const uint32_t off_q = (kk >> 2) * CHUNK + (kk & 3) * 32;
@@ -634,18 +671,18 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ 
           tc::mma_commit(&s_full[b]);
         }
         if (j >= 1) {
-          const int b = (j - 1) & 1;
+          const int b = (j - 1) & 1, st = (j - 1) % KST;
           const uint32_t ph = ((j - 1) >> 1) & 1;
           tc::mbar_wait(&ds_full[b], ph);
           tc::tc_fence_after();
-          const uint32_t ds = tc::smem_u32(sdS + b * DS_T), k_base = tc::smem_u32(sK + b * K_T);
+          const uint32_t ds = tc::smem_u32(sdS + b * DS_T), k_base = tc::smem_u32(sK + st * K_T);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)  // K = 64 keys
             tc::mma_bf16_ss(tmem + 256, tc::smem_desc(ds + kk * 32, 16, 1024, tc::kSwizzle128B),
                             tc::smem_desc(k_base + kk * 2048, KCH, 1024, tc::kSwizzle128B), idesc_q,
                             (j - 1) > 0 || kk > 0);
           tc::mma_commit(&ds_empty[b]);
-          tc::mma_commit(&kv_empty[b]);
+          tc::mma_commit(&kv_empty[st]);
         }
       }
       tc::mma_commit(done);
@@ -676,6 +713,7 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ 
       tc::mbar_arrive(&s_empty[b]);
       tc::mbar_wait(&ds_empty[b], ph ^ 1);
       uint8_t* tile = sdS + b * DS_T;
+      const bool full_blk = __all_sync(0xffffffffu, lim >= 63);
 #pragma unroll
       for (int c32 = 0; c32 < 2; ++c32) {
         uint32_t w[16];
@@ -685,7 +723,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ 
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int c = c32 * 32 + e + u;
-            const float pr = (c <= lim) ? exp2f(__uint_as_float(sv[c]) * p.scale_log2 - lse2) : 0.f;
+            float pr = ex2(fmaf(__uint_as_float(sv[c]), p.scale_log2, -lse2));
+            if (!full_blk && c > lim) pr = 0.f;
             d2[u] = pr * (__uint_as_float(dpv[c]) - dlt);
           }
           w[e / 2] = pack_bf16(d2[0], d2[1]);
@@ -813,8 +852,10 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
   auto run = [&](auto hd_tag) {
     constexpr int HD = decltype(hd_tag)::value;
     constexpr int NC = (HD + 63) / 64;
-    const size_t smem_dkv = 2 * NC * CHUNK + 4 * (NC * CHUNK / 2) + 4 * CHUNK + 1024 + 1024 + 256;
-    const size_t smem_dq = 2 * NC * CHUNK + 4 * (NC * CHUNK / 2) + 2 * CHUNK + 1024 + 256;
+    constexpr int QST = NC == 1 ? 4 : 3, KST = 4;
+    const size_t smem_dkv = 2 * NC * CHUNK + 2 * QST * (NC * CHUNK / 2) + 4 * CHUNK + QST * 512 + (10 + 2 * QST) * 8 + 8 +
+                            1024;
+    const size_t smem_dq = 2 * NC * CHUNK + 2 * KST * (NC * CHUNK / 2) + 2 * CHUNK + (6 + 2 * KST) * 8 + 8 + 1024;
     SPK_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dkv));
     SPK_CUDA(cudaFuncSetAttribute(attn_bwd_dq_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dq));
     dim3 g1(static_cast<unsigned>((kv_len + 127) / 128), static_cast<unsigned>(H));
