@@ -198,6 +198,23 @@ int sp_device_partition(const sp_scenario* cfg, int32_t mode, int32_t cuda_devic
 int sp_device_schedule_ops(const sp_scenario* cfg, int32_t kind, int32_t cuda_device, sp_task* ops,
                            int64_t* counts);
 
+/* ---- pipeline P2P plan (what the multi-process engine sends / receives) ---- */
+enum { SP_COMM_SEND = 0, SP_COMM_RECV = 1 };
+typedef struct sp_comm_op {
+  int32_t op_index;   /* position in the device order                               */
+  int32_t when;       /* 0: before the op (receive), 1: after the op (send)           */
+  int32_t dir;        /* SP_COMM_SEND / SP_COMM_RECV                                  */
+  int32_t peer;       /* peer rank (device - 1)                                       */
+  int32_t channel;    /* 0/1 activations (even/odd edge), 2/3 gradients               */
+  int32_t kind;       /* task kind of the op                                          */
+  int32_t micro_batch, segment, stage;
+  int32_t reserved;
+  int64_t elems;      /* segment_tokens * hidden                                      */
+} sp_comm_op;
+/* Size query with out == NULL. device is 1-based. */
+int sp_comm_plan(const sp_scenario* cfg, int32_t schedule_kind, const int64_t* lengths, int32_t device,
+                 int64_t hidden, sp_comm_op* out, int64_t* n);
+
 /* ---- execution engine ---- */
 enum { SP_MODEL_GPT = 0, SP_MODEL_LLAMA = 1 };
 enum { SP_DTYPE_F32 = 0, SP_DTYPE_BF16 = 1 };

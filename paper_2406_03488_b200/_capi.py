@@ -83,8 +83,15 @@ class StepReport(C.Structure):
     ]
 
 
+class CommOp(C.Structure):
+    _fields_ = [("op_index", C.c_int32), ("when", C.c_int32), ("dir", C.c_int32), ("peer", C.c_int32),
+                ("channel", C.c_int32), ("kind", C.c_int32), ("micro_batch", C.c_int32), ("segment", C.c_int32),
+                ("stage", C.c_int32), ("reserved", C.c_int32), ("elems", C.c_int64)]
+
+
 P = C.POINTER
 _SIGS = {
+    "sp_comm_plan": (C.c_int, [P(Scenario), C.c_int32, P(C.c_int64), C.c_int32, C.c_int64, P(CommOp), P(C.c_int64)]),
     "sp_last_error": (C.c_char_p, []),
     "sp_version": (C.c_char_p, []),
     "sp_scenario_default": (None, [P(Scenario)]),

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "capi/capi_common.hpp"
+#include "engine/comm_plan.hpp"
 #include "engine/engine.hpp"
 #include "seqpipe_b200.h"
 
@@ -85,6 +86,22 @@ int sp_engine_create(const sp_scenario* cfg, int32_t schedule_kind, const int64_
     eng->impl = std::make_unique<spe::Engine>(c, spc::kind_from_c(schedule_kind), part.lengths, model_from_c(model),
                                               rank, world_size, cuda_device);
     *out = eng.release();
+  });
+}
+
+int sp_comm_plan(const sp_scenario* cfg, int32_t schedule_kind, const int64_t* lengths, int32_t device, int64_t hidden,
+                 sp_comm_op* out, int64_t* n) {
+  return eguard([&] {
+    auto c = spc::from_c(cfg);
+    auto part = spc::partition_from_c(c, lengths, c.segments);
+    if (device < 1 || device > c.pipeline_size) throw std::out_of_range("device out of range");
+    auto sch = seqpipe::generate(c, spc::kind_from_c(schedule_kind), part);
+    auto plan = spe::comm_plan(sch, part.lengths, device, hidden);
+    if (out) {
+      if (*n < static_cast<int64_t>(plan.size())) throw spc::SpStatusError(SP_ERR_BUFFER_TOO_SMALL, "buffer too small");
+      std::copy(plan.begin(), plan.end(), out);
+    }
+    *n = static_cast<int64_t>(plan.size());
   });
 }
 

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstring>
 
+#include "engine/comm_plan.hpp"
 #include "seqpipe/sim.hpp"
 #include "seqpipe/validate.hpp"
 
@@ -66,6 +67,10 @@ Engine::Engine(const seqpipe::ScenarioConfig& cfg, seqpipe::ScheduleKind kind, c
   } else {
     const auto& order = sched_.device_orders[static_cast<size_t>(rank_)];
     for (size_t j = 0; j < order.size(); ++j) replay_.emplace_back(rank_, static_cast<int>(j));
+    plan_pre_.assign(order.size(), {});
+    plan_post_.assign(order.size(), {});
+    for (const sp_comm_op& c : comm_plan(sched_, len_, rank_ + 1, mc_.h))
+      (c.when == 0 ? plan_pre_ : plan_post_)[static_cast<size_t>(c.op_index)].push_back(c);
   }
   // In-process stage hand-off: stage v's layer-0 input aliases stage v-1's output.
   for (auto& [v, st] : stages_) {
@@ -138,67 +143,63 @@ void Engine::comm_init(const std::vector<std::string>& ids) {
 
 static ncclDataType_t nccl_type(DType t) { return t == DType::kF32 ? ncclFloat32 : ncclBfloat16; }
 
-void Engine::exec_op(const seqpipe::Task& t, int i) {
+// Executes op `t` (position `pos` of its device order, `i`-th op of this step).
+// Multi-process: the transfers are exactly sp_comm_plan's entries for this op —
+// receives on s_recv_ before the op (the compute stream waits on them), sends
+// on s_send_ after it (the compute stream never waits on a send).
+void Engine::exec_op(const seqpipe::Task& t, int i, int pos) {
   Stage* st = stage_obj(t.stage);
-  const int V = cfg_.total_stages();
-  const int P = cfg_.pipeline_size;
-  auto remote = [&](int other_stage) { return !stages_.count(other_stage); };
   Stage::Seg& sg = st->seg(t.micro_batch, t.segment);
-  const size_t bytes_elems = static_cast<size_t>(sg.n) * mc_.h;
-  if (t.kind == seqpipe::TaskKind::kForward) {
-    if (t.stage > 1 && remote(t.stage - 1)) {
-      // activation edge (v-1 -> v): communicator parity of the lower stage
-      const int ci = (t.stage - 1) % 2;
-      const int peer = (t.stage - 2) % P;
-      SPK_CUDA(cudaEventRecord(ev_tmp_, s_));  // x_in[0] region is free once earlier ops retired
+  const bool fwd = t.kind == seqpipe::TaskKind::kForward;
+  if (t.kind != seqpipe::TaskKind::kForward && t.kind != seqpipe::TaskKind::kFusedBackward)
+    throw std::invalid_argument("engine executes F and B tasks only");
+  const std::vector<sp_comm_op>* pre = nullptr;
+  const std::vector<sp_comm_op>* post = nullptr;
+  if (world_ > 1) {
+    pre = &plan_pre_[static_cast<size_t>(pos)];
+    post = &plan_post_[static_cast<size_t>(pos)];
+  }
+  if (pre) {
+    for (const sp_comm_op& c : *pre) {  // receive into this op's input buffer
+      SPK_CUDA(cudaEventRecord(ev_tmp_, s_));  // buffer region free once earlier ops retired
       SPK_CUDA(cudaStreamWaitEvent(s_recv_, ev_tmp_));
-      SPE_NCCL(ncclRecv(sg.x_in[0], bytes_elems, nccl_type(mc_.dt), peer, comms_[ci], s_recv_));
+      SPE_NCCL(ncclRecv(fwd ? sg.x_in[0] : sg.dy_in, static_cast<size_t>(c.elems), nccl_type(mc_.dt), c.peer,
+                        comms_[c.channel], s_recv_));
       SPK_CUDA(cudaEventRecord(ev_tmp_, s_recv_));
       SPK_CUDA(cudaStreamWaitEvent(s_, ev_tmp_));
     }
+  }
+  if (fwd) {
     SPK_CUDA(cudaEventRecord(ev_start_[i], s_));
     st->forward(t.micro_batch, t.segment, tokens_dev_, loss_dev_, 1.0f / (float)(cfg_.micro_batches * cfg_.seq_len));
     SPK_CUDA(cudaEventRecord(ev_end_[i], s_));
-    if (t.stage < V && remote(t.stage + 1)) {
-      const int ci = t.stage % 2;
-      const int peer = t.stage % P;
-      SPK_CUDA(cudaStreamWaitEvent(s_send_, ev_end_[i]));
-      SPE_NCCL(ncclSend(sg.x_out, bytes_elems, nccl_type(mc_.dt), peer, comms_[ci], s_send_));
-    }
-  } else if (t.kind == seqpipe::TaskKind::kFusedBackward) {
-    if (t.stage < V && remote(t.stage + 1)) {
-      const int ci = 2 + t.stage % 2;
-      const int peer = t.stage % P;
-      SPK_CUDA(cudaEventRecord(ev_tmp_, s_));
-      SPK_CUDA(cudaStreamWaitEvent(s_recv_, ev_tmp_));
-      SPE_NCCL(ncclRecv(sg.dy_in, bytes_elems, nccl_type(mc_.dt), peer, comms_[ci], s_recv_));
-      SPK_CUDA(cudaEventRecord(ev_tmp_, s_recv_));
-      SPK_CUDA(cudaStreamWaitEvent(s_, ev_tmp_));
-    }
-    void* dx_target = nullptr;
-    int slot = -1;
-    if (t.stage > 1) {
-      if (remote(t.stage - 1)) {
-        slot = send_ring_next_;
-        send_ring_next_ = (send_ring_next_ + 1) % static_cast<int>(send_ring_.size());
-        SPK_CUDA(cudaStreamWaitEvent(s_, send_ring_ev_[static_cast<size_t>(slot)]));
-        dx_target = send_ring_[static_cast<size_t>(slot)];
-      } else {
-        dx_target = stage_obj(t.stage - 1)->seg(t.micro_batch, t.segment).dy_in;
+    if (post)
+      for (const sp_comm_op& c : *post) {
+        SPK_CUDA(cudaStreamWaitEvent(s_send_, ev_end_[i]));
+        SPE_NCCL(ncclSend(sg.x_out, static_cast<size_t>(c.elems), nccl_type(mc_.dt), c.peer, comms_[c.channel],
+                          s_send_));
       }
-    }
-    SPK_CUDA(cudaEventRecord(ev_start_[i], s_));
-    st->backward(t.micro_batch, t.segment, dx_target, tokens_dev_);
-    SPK_CUDA(cudaEventRecord(ev_end_[i], s_));
-    if (slot >= 0) {
-      const int ci = 2 + (t.stage - 1) % 2;
-      const int peer = (t.stage - 2) % P;
+    return;
+  }
+  void* dx_target = nullptr;
+  int slot = -1;
+  if (post && !post->empty()) {
+    slot = send_ring_next_;
+    send_ring_next_ = (send_ring_next_ + 1) % static_cast<int>(send_ring_.size());
+    SPK_CUDA(cudaStreamWaitEvent(s_, send_ring_ev_[static_cast<size_t>(slot)]));
+    dx_target = send_ring_[static_cast<size_t>(slot)];
+  } else if (t.stage > 1) {
+    dx_target = stage_obj(t.stage - 1)->seg(t.micro_batch, t.segment).dy_in;  // in-process hand-off
+  }
+  SPK_CUDA(cudaEventRecord(ev_start_[i], s_));
+  st->backward(t.micro_batch, t.segment, dx_target, tokens_dev_);
+  SPK_CUDA(cudaEventRecord(ev_end_[i], s_));
+  if (slot >= 0) {
+    for (const sp_comm_op& c : *post) {
       SPK_CUDA(cudaStreamWaitEvent(s_send_, ev_end_[i]));
-      SPE_NCCL(ncclSend(dx_target, bytes_elems, nccl_type(mc_.dt), peer, comms_[ci], s_send_));
-      SPK_CUDA(cudaEventRecord(send_ring_ev_[static_cast<size_t>(slot)], s_send_));
+      SPE_NCCL(ncclSend(dx_target, static_cast<size_t>(c.elems), nccl_type(mc_.dt), c.peer, comms_[c.channel], s_send_));
     }
-  } else {
-    throw std::invalid_argument("engine executes F and B tasks only");
+    SPK_CUDA(cudaEventRecord(send_ring_ev_[static_cast<size_t>(slot)], s_send_));
   }
 }
 
@@ -227,7 +228,7 @@ void Engine::step(const int32_t* tokens, bool on_device, sp_step_report* rep) {
   for (size_t i = 0; i < replay_.size(); ++i) {
     const auto [d, j] = replay_[i];
     const seqpipe::Task& t = sched_.device_orders[static_cast<size_t>(d)][static_cast<size_t>(j)];
-    exec_op(t, static_cast<int>(i));
+    exec_op(t, static_cast<int>(i), j);
     op_log_.push_back(t);
   }
   if (s_send_) {  // the step ends when this device's sends have drained

@@ -210,7 +210,8 @@ class Engine {
   }
 
  private:
-  void exec_op(const seqpipe::Task& t, int order_index);
+  void exec_op(const seqpipe::Task& t, int order_index, int device_pos);
+  std::vector<std::vector<sp_comm_op>> plan_pre_, plan_post_;  // per device-order position
   Stage* stage_obj(int stage) { return stages_.at(stage).get(); }
 
   seqpipe::ScenarioConfig cfg_;

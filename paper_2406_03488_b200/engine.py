@@ -169,6 +169,23 @@ def plan_memory(cfg: pl.ScenarioConfig, kind, partition: pl.SequencePartition, m
     return a.value, b.value, d.value
 
 
+def comm_plan(cfg: pl.ScenarioConfig, kind, partition: pl.SequencePartition, device: int, hidden: int):
+    """P2P transfers the multi-process engine issues on `device` (1-based), in issue order:
+    list of dicts (op_index, when 'pre'/'post', dir 'send'/'recv', peer rank, channel, task, elems)."""
+    c = cfg.to_c()
+    lens = (C.c_int64 * len(partition.lengths))(*partition.lengths)
+    n = C.c_int64(0)
+    _check(_capi.lib().sp_comm_plan(C.byref(c), pl.kind_id(kind), lens, device, hidden, None, C.byref(n)))
+    buf = (_capi.CommOp * max(1, n.value))()
+    _check(_capi.lib().sp_comm_plan(C.byref(c), pl.kind_id(kind), lens, device, hidden, buf, C.byref(n)))
+    out = []
+    for o in buf[: n.value]:
+        out.append({"op_index": o.op_index, "when": "pre" if o.when == 0 else "post",
+                    "dir": "send" if o.dir == 0 else "recv", "peer": o.peer, "channel": o.channel,
+                    "task": (pl.TASK_KINDS[o.kind], o.micro_batch, o.segment, o.stage), "elems": o.elems})
+    return out
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(_capi.lib().sp_nccl_unique_id(buf, 128))
