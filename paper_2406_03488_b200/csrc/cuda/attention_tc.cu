@@ -330,7 +330,7 @@ struct __align__(64) AttnBwdParams {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__ AttnBwdParams p) {
+__global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__ AttnBwdParams p) {
   constexpr int NC = (HD + 63) / 64;
   constexpr int KV_T = NC * CHUNK;       // [128 rows x hd] tile
   constexpr int Q_T = NC * CHUNK / 2;    // [64 rows x hd] tile (chunks of 8 KB)
@@ -372,8 +372,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
     tc::mbar_init(done, 1);
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&s_empty[i], 128);
-      tc::mbar_init(&p_full[i], 128);
+      tc::mbar_init(&s_empty[i], 256);
+      tc::mbar_init(&p_full[i], 256);
       tc::mbar_init(&p_empty[i], 1);
     }
     for (int i = 0; i < QST; ++i) {
@@ -474,7 +474,9 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
       tc::mma_commit(done);
     }
   } else if (warp >= 4) {
-    const int quarter = warp & 3;
+    // 8 softmax warps: warps w and w+4 share TMEM lane quarter w%4 (one key row
+    // per lane) and split the 64 query columns in halves -> two warps per SMSP.
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
     const int r = quarter * 32 + lane;  // key row
     const int64_t kpos = j0 + r;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
@@ -482,52 +484,46 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
       const int b = it & 1, st = it % QST;
       const uint32_t ph = (it >> 1) & 1;
       const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
-      const float* ld = sLD + st * 128;
+      const float* ld = sLD + st * 128 + half * 32;
       tc::mbar_wait(&q_full[st], (it / QST) & 1);  // LSE / delta of this block are in SMEM
-      // visible query columns c: q_off + i0 + c >= kpos and i0 + c < n
-      int64_t cmin = kpos - p.q_off - i0;
-      const int c_lo = cmin < 0 ? 0 : (cmin > 64 ? 64 : static_cast<int>(cmin));
-      const int c_hi = static_cast<int>((p.n - i0) < 64 ? (p.n - i0) : 64);  // exclusive
+      // visible query columns c (local to this half): q_off + i0 + 32*half + c >= kpos, i0 + 32*half + c < n
+      const int64_t cbase = i0 + half * 32;
+      int64_t cmin = kpos - p.q_off - cbase;
+      const int c_lo = cmin < 0 ? 0 : (cmin > 32 ? 32 : static_cast<int>(cmin));
+      const int64_t chi = p.n - cbase;
+      const int c_hi = chi < 0 ? 0 : (chi > 32 ? 32 : static_cast<int>(chi));  // exclusive
       tc::mbar_wait(&s_full[b], ph);
       tc::tc_fence_after();
-      uint32_t sv[64], dpv[64];
-      tc::tmem_ld32(tmem + lane_base + b * 64, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
-      tc::tmem_ld32(tmem + lane_base + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
-      tc::tmem_ld32(tmem + lane_base + 128 + b * 64, *reinterpret_cast<uint32_t(*)[32]>(&dpv[0]));
-      tc::tmem_ld32(tmem + lane_base + 128 + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&dpv[32]));
+      uint32_t sv[32], dpv[32];
+      tc::tmem_ld32(tmem + lane_base + b * 64 + half * 32, sv);
+      tc::tmem_ld32(tmem + lane_base + 128 + b * 64 + half * 32, dpv);
       tc::tmem_ld_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&s_empty[b]);
       tc::mbar_wait(&p_empty[b], ph ^ 1);
-      uint8_t* ptile = sPt + b * PT;
-      uint8_t* dstile = sdSt + b * PT;
-      const bool full_blk = __all_sync(0xffffffffu, c_lo == 0 && c_hi == 64);
+      const bool full_blk = __all_sync(0xffffffffu, c_lo == 0 && c_hi == 32);
+      uint32_t wp[16], wd[16];
 #pragma unroll
-      for (int c32 = 0; c32 < 2; ++c32) {
-        uint32_t wp[16], wd[16];
+      for (int e = 0; e < 32; e += 4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(ld + e);       // LSE (log2) of 4 queries
+        const float4 d4 = *reinterpret_cast<const float4*>(ld + 64 + e);  // delta of 4 queries
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
+        float pv[4], dv[4];
 #pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const int c0 = c32 * 32 + e;
-          const float4 l4 = *reinterpret_cast<const float4*>(ld + c0);       // LSE (log2) of 4 queries
-          const float4 d4 = *reinterpret_cast<const float4*>(ld + 64 + c0);  // delta of 4 queries
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
-          float pv[4], dv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int c = c0 + u;
-            float pr = ex2(fmaf(__uint_as_float(sv[c]), p.scale_log2, -lv[u]));
-            if (!full_blk && (c < c_lo || c >= c_hi)) pr = 0.f;
-            pv[u] = pr;
-            dv[u] = pr * (__uint_as_float(dpv[c]) - dl[u]);
-          }
-          wp[e / 2] = pack_bf16(pv[0], pv[1]);
-          wp[e / 2 + 1] = pack_bf16(pv[2], pv[3]);
-          wd[e / 2] = pack_bf16(dv[0], dv[1]);
-          wd[e / 2 + 1] = pack_bf16(dv[2], dv[3]);
+        for (int u = 0; u < 4; ++u) {
+          const int c = e + u;
+          float pr = ex2(fmaf(__uint_as_float(sv[c]), p.scale_log2, -lv[u]));
+          if (!full_blk && (c < c_lo || c >= c_hi)) pr = 0.f;
+          pv[u] = pr;
+          dv[u] = pr * (__uint_as_float(dpv[c]) - dl[u]);
         }
-        st_tile_row32(ptile, r, c32, wp);
-        st_tile_row32(dstile, r, c32, wd);
+        wp[e / 2] = pack_bf16(pv[0], pv[1]);
+        wp[e / 2 + 1] = pack_bf16(pv[2], pv[3]);
+        wd[e / 2] = pack_bf16(dv[0], dv[1]);
+        wd[e / 2 + 1] = pack_bf16(dv[2], dv[3]);
       }
+      st_tile_row32(sPt + b * PT, r, half, wp);
+      st_tile_row32(sdSt + b * PT, r, half, wd);
       fence_async_smem();
       tc::mbar_arrive(&p_full[b]);
     }
@@ -536,8 +532,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
     const bool own = kpos < p.kv_len;
     float* dk_row = p.dkv + (own ? kpos : 0) * 2 * p.h + head * HD;
     float* dv_row = dk_row + p.h;
-#pragma unroll
-    for (int c = 0; c < HD / 16; ++c) {
+    constexpr int NCH = HD / 16, SPLIT = (NCH + 1) / 2;
+    for (int c = half ? SPLIT : 0; c < (half ? NCH : SPLIT); ++c) {
       uint32_t v[16], k[16];
       // tcgen05.ld is warp-collective: every lane loads, only owners store.
       tmem_ld16(tmem + lane_base + 256 + c * 16, v);
@@ -569,7 +565,7 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_k(const __grid_constant__
 }
 
 template <int HD>
-__global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ AttnBwdParams p) {
+__global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ AttnBwdParams p) {
   constexpr int NC = (HD + 63) / 64;
   constexpr int Q_T = NC * CHUNK;        // [128 rows x hd]
   constexpr int K_T = NC * CHUNK / 2;    // [64 rows x hd]
@@ -608,8 +604,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ 
     tc::mbar_init(done, 1);
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&s_empty[i], 128);
-      tc::mbar_init(&ds_full[i], 128);
+      tc::mbar_init(&s_empty[i], 256);
+      tc::mbar_init(&ds_full[i], 256);
       tc::mbar_init(&ds_empty[i], 1);
     }
     for (int i = 0; i < KST; ++i) {
@@ -688,7 +684,9 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ 
       tc::mma_commit(done);
     }
   } else if (warp >= 4) {
-    const int quarter = warp & 3;
+    // 8 softmax warps: warps w and w+4 share lane quarter w%4 (one query row per
+    // lane) and split the 64 key columns of each block in halves.
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
     const int r = quarter * 32 + lane;
     const int64_t row = q0 + r;
     const bool valid = row < p.n;
@@ -699,38 +697,33 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ 
     for (int j = 0; j < nblk; ++j) {
       const int b = j & 1;
       const uint32_t ph = (j >> 1) & 1;
-      const int64_t lim64 = valid ? qpos - static_cast<int64_t>(j) * 64 : -1;  // key columns <= lim visible
+      // key columns c (local to this half) with j*64 + 32*half + c <= qpos are visible
+      const int64_t lim64 = valid ? qpos - static_cast<int64_t>(j) * 64 - half * 32 : -1;
       const int lim = lim64 > 1000 ? 1000 : static_cast<int>(lim64);
       tc::mbar_wait(&s_full[b], ph);
       tc::tc_fence_after();
-      uint32_t sv[64], dpv[64];
-      tc::tmem_ld32(tmem + lane_base + b * 64, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
-      tc::tmem_ld32(tmem + lane_base + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
-      tc::tmem_ld32(tmem + lane_base + 128 + b * 64, *reinterpret_cast<uint32_t(*)[32]>(&dpv[0]));
-      tc::tmem_ld32(tmem + lane_base + 128 + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&dpv[32]));
+      uint32_t sv[32], dpv[32];
+      tc::tmem_ld32(tmem + lane_base + b * 64 + half * 32, sv);
+      tc::tmem_ld32(tmem + lane_base + 128 + b * 64 + half * 32, dpv);
       tc::tmem_ld_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&s_empty[b]);
       tc::mbar_wait(&ds_empty[b], ph ^ 1);
-      uint8_t* tile = sdS + b * DS_T;
-      const bool full_blk = __all_sync(0xffffffffu, lim >= 63);
+      const bool full_blk = __all_sync(0xffffffffu, lim >= 31);
+      uint32_t w[16];
 #pragma unroll
-      for (int c32 = 0; c32 < 2; ++c32) {
-        uint32_t w[16];
+      for (int e = 0; e < 32; e += 2) {
+        float d2[2];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float d2[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int c = c32 * 32 + e + u;
-            float pr = ex2(fmaf(__uint_as_float(sv[c]), p.scale_log2, -lse2));
-            if (!full_blk && c > lim) pr = 0.f;
-            d2[u] = pr * (__uint_as_float(dpv[c]) - dlt);
-          }
-          w[e / 2] = pack_bf16(d2[0], d2[1]);
+        for (int u = 0; u < 2; ++u) {
+          const int c = e + u;
+          float pr = ex2(fmaf(__uint_as_float(sv[c]), p.scale_log2, -lse2));
+          if (!full_blk && c > lim) pr = 0.f;
+          d2[u] = pr * (__uint_as_float(dpv[c]) - dlt);
         }
-        st_tile_row32(tile, r, c32, w);
+        w[e / 2] = pack_bf16(d2[0], d2[1]);
       }
+      st_tile_row32(sdS + b * DS_T, r, half, w);
       fence_async_smem();
       tc::mbar_arrive(&ds_full[b]);
     }
@@ -738,8 +731,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_k(const __grid_constant__ 
     tc::tc_fence_after();
     {
       __nv_bfloat16* dq_row = p.dq + (valid ? row : 0) * p.h + head * HD;
-#pragma unroll
-      for (int c = 0; c < HD / 16; ++c) {
+      constexpr int NCH = HD / 16, SPLIT = (NCH + 1) / 2;
+      for (int c = half ? SPLIT : 0; c < (half ? NCH : SPLIT); ++c) {
         uint32_t v[16];
         tmem_ld16(tmem + lane_base + 256 + c * 16, v);  // warp-collective: all lanes
         tc::tmem_ld_wait();
@@ -859,10 +852,10 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
     SPK_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dkv));
     SPK_CUDA(cudaFuncSetAttribute(attn_bwd_dq_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dq));
     dim3 g1(static_cast<unsigned>((kv_len + 127) / 128), static_cast<unsigned>(H));
-    attn_bwd_dkv_k<HD><<<g1, 256, smem_dkv, s>>>(a);
+    attn_bwd_dkv_k<HD><<<g1, 384, smem_dkv, s>>>(a);
     SPK_LAUNCH_CHECK();
     dim3 g2(static_cast<unsigned>((n + 127) / 128), static_cast<unsigned>(H));
-    attn_bwd_dq_k<HD><<<g2, 256, smem_dq, s>>>(b);
+    attn_bwd_dq_k<HD><<<g2, 384, smem_dq, s>>>(b);
     SPK_LAUNCH_CHECK();
   };
   switch (hd) {
