@@ -66,9 +66,9 @@ int sp_attention_bwd(int32_t dtype, int32_t impl, const void* q, const void* kv,
   return cuda_guard([&] {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     float* ws = nullptr;
-    const size_t floats = static_cast<size_t>(n) * heads + static_cast<size_t>(n) * heads * head_dim;
+    const size_t floats = spk::attn_bwd_ws_delta_floats(n, heads) + static_cast<size_t>(n) * heads * head_dim;
     SPK_CUDA(cudaMallocAsync(&ws, floats * sizeof(float), s));
-    spk::attn_bwd(dt(dtype), impl, q, kv, o, dout, lse, ws, ws + static_cast<size_t>(n) * heads, dq, dkv_acc, n, q_off,
+    spk::attn_bwd(dt(dtype), impl, q, kv, o, dout, lse, ws, ws + spk::attn_bwd_ws_delta_floats(n, heads), dq, dkv_acc, n, q_off,
                   kv_len, heads, head_dim, s);
     SPK_CUDA(cudaFreeAsync(ws, s));
   });

@@ -16,6 +16,7 @@
 // TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "cuda/common.cuh"
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
   uint64_t* p_full = bars + 11;  // [2]
   uint64_t* p_empty = bars + 13; // [2]
   uint64_t* o_done = bars + 15;  // one phase per PV MMA group
+  uint64_t* v_empty = bars + 16; // [2]  (kv_empty above now releases K stages only)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
       tc::mbar_init(&k_full[i], 1);
       tc::mbar_init(&v_full[i], 1);
       tc::mbar_init(&kv_empty[i], 1);
+      tc::mbar_init(&v_empty[i], 1);
       tc::mbar_init(&s_full[i], 1);
       tc::mbar_init(&s_empty[i], 128);
       tc::mbar_init(&p_full[i], 128);
@@ -133,12 +136,20 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
       tc::mbar_expect_tx(q_full, QBYTES);
       for (int c = 0; c < NC; ++c)
         tc::tma_load_2d(sQ + c * CHUNK, &p.tq, q_full, head * HD + 64 * c, static_cast<int>(q0));
-      for (int j = 0; j < nblk; ++j) {
+      // K runs one block ahead of V: K_{j+1} (freed after S_{j-1}) is requested
+      // before V_j (freed after PV_{j-2}) so a slow PV never starves S.
+      auto load_k = [&](int j) {
         const int st = j & 1;
         tc::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
         tc::mbar_expect_tx(&k_full[st], KBYTES);
         for (int c = 0; c < NC; ++c)
           tc::tma_load_2d(sK + st * KBYTES + c * CHUNK, &p.tkv, &k_full[st], head * HD + 64 * c, j * BKV);
+      };
+      if (nblk > 0) load_k(0);
+      for (int j = 0; j < nblk; ++j) {
+        if (j + 1 < nblk) load_k(j + 1);
+        const int st = j & 1;
+        tc::mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
         tc::mbar_expect_tx(&v_full[st], VBYTES);
         for (int c = 0; c < NC; ++c)
           tc::tma_load_2d(sV + st * VBYTES + c * CHUNK, &p.tkv, &v_full[st], p.h + head * HD + 64 * c, j * BKV);
@@ -150,12 +161,14 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
       constexpr uint32_t idesc_o = tc::idesc_bf16(128, HD, false, true);
       tc::mbar_wait(q_full, 0);
       const uint32_t q_base = tc::smem_u32(sQ);
-      for (int j = 0; j <= nblk; ++j) {
-        if (j < nblk) {
-          const int b = j & 1;
-          const uint32_t ph = (j >> 1) & 1;
-          tc::mbar_wait(&k_full[b], ph);
-          tc::mbar_wait(&s_empty[b], ph ^ 1);
+      // Poll two queues: S_j (needs K_j and a free S buffer) and PV_j (needs P_j
+      // and V_j). K and V stages are released separately (K after S_j, V after
+      // PV_j), so S can run two blocks ahead of the softmax.
+      int sj = 0, pj = 0;
+      while (pj < nblk) {
+        if (sj < nblk && tc::mbar_test(&k_full[sj & 1], (sj >> 1) & 1) &&
+            tc::mbar_test(&s_empty[sj & 1], ((sj >> 1) & 1) ^ 1)) {
+          const int b = sj & 1;
           tc::tc_fence_after();
           const uint32_t k_base = tc::smem_u32(sK + b * KBYTES);
 #pragma unroll
@@ -165,12 +178,12 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
                             tc::smem_desc(k_base + off, 16, 1024, tc::kSwizzle128B), idesc_s, kk > 0);
           }
           tc::mma_commit(&s_full[b]);
+          tc::mma_commit(&kv_empty[b]);  // K stage free
+          ++sj;
+          continue;
         }
-        if (j >= 1) {
-          const int b = (j - 1) & 1;
-          const uint32_t ph = ((j - 1) >> 1) & 1;
-          tc::mbar_wait(&p_full[b], ph);
-          tc::mbar_wait(&v_full[b], ph);
+        if (pj < sj && tc::mbar_test(&p_full[pj & 1], (pj >> 1) & 1) && tc::mbar_test(&v_full[pj & 1], (pj >> 1) & 1)) {
+          const int b = pj & 1;
           tc::tc_fence_after();
           const uint32_t p_base = tc::smem_u32(sP + b * PBYTES);
           const uint32_t v_base = tc::smem_u32(sV + b * VBYTES);
@@ -178,11 +191,12 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
           for (int kk = 0; kk < BKV / 16; ++kk) {
             const uint64_t ad = tc::smem_desc(p_base + (kk >> 2) * CHUNK + (kk & 3) * 32, 16, 1024, tc::kSwizzle128B);
             const uint64_t bd = tc::smem_desc(v_base + kk * 2048, CHUNK, 1024, tc::kSwizzle128B);
-            tc::mma_bf16_ss(tmem + 256, ad, bd, idesc_o, (j - 1) > 0 || kk > 0);  // O accumulates in TMEM
+            tc::mma_bf16_ss(tmem + 256, ad, bd, idesc_o, pj > 0 || kk > 0);  // O accumulates in TMEM
           }
           tc::mma_commit(o_done);
           tc::mma_commit(&p_empty[b]);
-          tc::mma_commit(&kv_empty[b]);
+          tc::mma_commit(&v_empty[b]);  // V stage free
+          ++pj;
         }
       }
     }
@@ -320,13 +334,14 @@ struct __align__(64) AttnBwdParams {
   CUtensorMap tq;    // q   [n, h]      box 64 rows
   CUtensorMap tdo;   // dO  [n, h]      box 64 rows (dKV kernel) / 128 rows (dQ kernel)
   CUtensorMap tkv;   // kv  [kv_len, 2h] box 128 rows (dKV kernel) / 64 rows (dQ kernel)
-  const float* lse;  // [H, n] natural log
-  const float* delta;  // [H, n]
+  const float* ld;     // [H, n_pad] x (LSE * log2e, delta), zero padded (attn_prep_k)
+  int64_t n_pad;       // n rounded up to 64
   float* dkv;        // [kv_len, 2h] fp32 accumulator
   __nv_bfloat16* dq; // [n, h]
   int64_t n, q_off, kv_len;
   int H, h;
   float scale, scale_log2;
+  int dbg;  // profiling only (SP_ATTN_DBG): 1 = skip MMAs, 2 = skip softmax math
 };
 
 template <int HD>
@@ -345,7 +360,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
   uint8_t* sdO = sQ + QST * Q_T;    // [QST]
   uint8_t* sPt = sdO + QST * Q_T;   // [2]
   uint8_t* sdSt = sPt + 2 * PT;     // [2]
-  float* sLD = reinterpret_cast<float*>(sdSt + 2 * PT);  // [QST][128]: lse*log2e (64), delta (64)
+  float* sLD = reinterpret_cast<float*>(sdSt + 2 * PT);  // [QST][64 x (lse*log2e, delta)]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + QST * 128);
   uint64_t* kv_full = bars;
   uint64_t* s_full = bars + 1;   // [2]
@@ -357,12 +372,18 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
   uint64_t* q_empty = q_full + QST;      // [QST]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + QST);
 
+  // 2-CTA cluster: CTAs own adjacent 128-key blocks and stream the same query
+  // blocks; each Q_i / dO_i tile is fetched once from L2 and multicast to both
+  // (rank 0 issues Q, rank 1 issues dO), halving the dominant L2 -> SMEM traffic.
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = tc::cluster_ctarank();
   const int num_kb = static_cast<int>((p.kv_len + 127) / 128);
-  const int kb = num_kb - 1 - static_cast<int>(blockIdx.x);
+  const int num_kb2 = (num_kb + 1) & ~1;
+  const int kb = num_kb2 - 1 - static_cast<int>(blockIdx.x);   // heaviest first; may be == num_kb (idle keys)
   const int head = blockIdx.y;
   const int64_t j0 = static_cast<int64_t>(kb) * 128;
-  int64_t ib0 = j0 - p.q_off;
+  const int64_t j0_lo = static_cast<int64_t>(num_kb2 - 2 - 2 * static_cast<int>(blockIdx.x / 2)) * 128;
+  int64_t ib0 = j0_lo - p.q_off;  // first query block any key of the pair can see (common to the cluster)
   if (ib0 < 0) ib0 = 0;
   ib0 = ib0 / 64 * 64;
   const int niter = static_cast<int>((p.n - ib0 + 63) / 64);
@@ -378,13 +399,13 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
     }
     for (int i = 0; i < QST; ++i) {
       tc::mbar_init(&q_full[i], 1);
-      tc::mbar_init(&q_empty[i], 1);
+      tc::mbar_init(&q_empty[i], 2);  // freed by both CTAs' MMA commits
     }
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
-  __syncthreads();
+  tc::cluster_sync();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // TMEM: S^T[2] at 0/64, dP^T[2] at 128/192, dV at 256, dK at 384.
@@ -402,30 +423,22 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
         tc::tma_load_2d(sV + c * CHUNK, &p.tkv, kv_full, p.h + head * HD + 64 * c, static_cast<int>(j0));
       }
     }
-    for (int it = 0; it < niter; ++it) {
-      const int st = it % QST;
-      const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
-      tc::mbar_wait(&q_empty[st], ((it / QST) & 1) ^ 1);
-      float* ld = sLD + st * 128;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int idx = lane + 32 * u;
-        const int64_t qi = i0 + (idx & 63);
-        float v = 0.f;
-        if (qi < p.n)
-          v = idx < 64 ? p.lse[static_cast<int64_t>(head) * p.n + qi] * 1.4426950408889634f
-                       : p.delta[static_cast<int64_t>(head) * p.n + qi];
-        ld[idx] = v;
-      }
-      __syncwarp();
-      if (lane == 0) {
-        tc::mbar_expect_tx(&q_full[st], 2 * Q_T);  // also publishes the LSE / delta stores
+    if (lane == 0) {
+      for (int it = 0; it < niter; ++it) {
+        const int st = it % QST;
+        const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
+        tc::mbar_wait(&q_empty[st], ((it / QST) & 1) ^ 1);  // stage free in both CTAs
+        tc::mbar_expect_tx(&q_full[st], 2 * Q_T + 512);
         for (int c = 0; c < NC; ++c) {
-          tc::tma_load_2d(sQ + st * Q_T + c * QCH, &p.tq, &q_full[st], head * HD + 64 * c, static_cast<int>(i0));
-          tc::tma_load_2d(sdO + st * Q_T + c * QCH, &p.tdo, &q_full[st], head * HD + 64 * c, static_cast<int>(i0));
+          if (rank == 0)
+            tc::tma_load_2d_mc(sQ + st * Q_T + c * QCH, &p.tq, &q_full[st], head * HD + 64 * c, static_cast<int>(i0), 3);
+          else
+            tc::tma_load_2d_mc(sdO + st * Q_T + c * QCH, &p.tdo, &q_full[st], head * HD + 64 * c, static_cast<int>(i0),
+                               3);
         }
+        // (LSE*log2e, delta) pairs of the 64 queries: one async 512-byte bulk copy
+        tc::bulk_load(sLD + st * 128, p.ld + (static_cast<int64_t>(head) * p.n_pad + i0) * 2, 512, &q_full[st]);
       }
-      __syncwarp();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -433,42 +446,51 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
       constexpr uint32_t idesc_g = tc::idesc_bf16(128, HD, false, true);
       tc::mbar_wait(kv_full, 0);
       const uint32_t k_base = tc::smem_u32(sK), v_base = tc::smem_u32(sV);
-      for (int it = 0; it <= niter; ++it) {
-        if (it < niter) {
+      // Two independent issue queues polled without blocking: S^T/dP^T of block
+      // s_it (needs its Q/dO stage and a free S buffer — released by the softmax
+      // warps right after their TMEM load) and dV/dK of block g_it (needs that
+      // block's P^T/dS^T). S can therefore run up to two blocks ahead of the
+      // softmax instead of waiting behind the previous dV/dK in program order.
+      int s_it = 0, g_it = 0;
+      while (g_it < niter) {
+        const bool s_ready = s_it < niter && tc::mbar_test(&q_full[s_it % QST], (s_it / QST) & 1) &&
+                             tc::mbar_test(&s_empty[s_it & 1], ((s_it >> 1) & 1) ^ 1);
+        if (s_ready) {
+          const int it = s_it++;
           const int b = it & 1, st = it % QST;
-          const uint32_t ph = (it >> 1) & 1;
-          tc::mbar_wait(&q_full[st], (it / QST) & 1);
-          tc::mbar_wait(&s_empty[b], ph ^ 1);
           tc::tc_fence_after();
           const uint32_t q_base = tc::smem_u32(sQ + st * Q_T), do_base = tc::smem_u32(sdO + st * Q_T);
+          if (!(p.dbg & 1)) {
 #pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint32_t off_kv = (kk >> 2) * CHUNK + (kk & 3) * 32;
-            const uint32_t off_q = (kk >> 2) * QCH + (kk & 3) * 32;
-            tc::mma_bf16_ss(tmem + b * 64, tc::smem_desc(k_base + off_kv, 16, 1024, tc::kSwizzle128B),
-                            tc::smem_desc(q_base + off_q, 16, 1024, tc::kSwizzle128B), idesc_s, kk > 0);
-            tc::mma_bf16_ss(tmem + 128 + b * 64, tc::smem_desc(v_base + off_kv, 16, 1024, tc::kSwizzle128B),
-                            tc::smem_desc(do_base + off_q, 16, 1024, tc::kSwizzle128B), idesc_s, kk > 0);
+            for (int kk = 0; kk < HD / 16; ++kk) {
+              const uint32_t off_kv = (kk >> 2) * CHUNK + (kk & 3) * 32;
+              const uint32_t off_q = (kk >> 2) * QCH + (kk & 3) * 32;
+              tc::mma_bf16_ss(tmem + b * 64, tc::smem_desc(k_base + off_kv, 16, 1024, tc::kSwizzle128B),
+                              tc::smem_desc(q_base + off_q, 16, 1024, tc::kSwizzle128B), idesc_s, kk > 0);
+              tc::mma_bf16_ss(tmem + 128 + b * 64, tc::smem_desc(v_base + off_kv, 16, 1024, tc::kSwizzle128B),
+                              tc::smem_desc(do_base + off_q, 16, 1024, tc::kSwizzle128B), idesc_s, kk > 0);
+            }
           }
           tc::mma_commit(&s_full[b]);
+          continue;
         }
-        if (it >= 1) {
-          const int b = (it - 1) & 1, st = (it - 1) % QST;
-          const uint32_t ph = ((it - 1) >> 1) & 1;
-          tc::mbar_wait(&p_full[b], ph);
+        if (g_it < s_it && tc::mbar_test(&p_full[g_it & 1], (g_it >> 1) & 1)) {
+          const int it = g_it++;
+          const int b = it & 1, st = it % QST;
           tc::tc_fence_after();
           const uint32_t pt = tc::smem_u32(sPt + b * PT), dst = tc::smem_u32(sdSt + b * PT);
           const uint32_t q_base = tc::smem_u32(sQ + st * Q_T), do_base = tc::smem_u32(sdO + st * Q_T);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries
-            const bool acc = (it - 1) > 0 || kk > 0;
+            if (p.dbg & 1) break;
+            const bool acc = it > 0 || kk > 0;
             tc::mma_bf16_ss(tmem + 256, tc::smem_desc(pt + kk * 32, 16, 1024, tc::kSwizzle128B),
                             tc::smem_desc(do_base + kk * 2048, QCH, 1024, tc::kSwizzle128B), idesc_g, acc);
             tc::mma_bf16_ss(tmem + 384, tc::smem_desc(dst + kk * 32, 16, 1024, tc::kSwizzle128B),
                             tc::smem_desc(q_base + kk * 2048, QCH, 1024, tc::kSwizzle128B), idesc_g, acc);
           }
           tc::mma_commit(&p_empty[b]);
-          tc::mma_commit(&q_empty[st]);
+          tc::mma_commit_mc(&q_empty[st], 3);  // this CTA is done with the multicast stage
         }
       }
       tc::mma_commit(done);
@@ -484,7 +506,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
       const int b = it & 1, st = it % QST;
       const uint32_t ph = (it >> 1) & 1;
       const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
-      const float* ld = sLD + st * 128 + half * 32;
+      const float* ld = sLD + st * 128 + half * 64;  // this half's 32 (lse, delta) pairs
       tc::mbar_wait(&q_full[st], (it / QST) & 1);  // LSE / delta of this block are in SMEM
       // visible query columns c (local to this half): q_off + i0 + 32*half + c >= kpos, i0 + 32*half + c < n
       const int64_t cbase = i0 + half * 32;
@@ -505,9 +527,10 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
       uint32_t wp[16], wd[16];
 #pragma unroll
       for (int e = 0; e < 32; e += 4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(ld + e);       // LSE (log2) of 4 queries
-        const float4 d4 = *reinterpret_cast<const float4*>(ld + 64 + e);  // delta of 4 queries
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
+        if (p.dbg & 2) break;
+        const float4 a4 = *reinterpret_cast<const float4*>(ld + 2 * e);      // (lse, delta) of queries e, e+1
+        const float4 b4 = *reinterpret_cast<const float4*>(ld + 2 * e + 4);  // (lse, delta) of queries e+2, e+3
+        const float lv[4] = {a4.x, a4.z, b4.x, b4.z}, dl[4] = {a4.y, a4.w, b4.y, b4.w};
         float pv[4], dv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -559,7 +582,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
     }
   }
   tc::tc_fence_before();
-  __syncthreads();
+  tc::cluster_sync();  // no multicast data / remote arrive may target an exited CTA
   tc::tc_fence_after();
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
@@ -647,12 +670,12 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ 
       constexpr uint32_t idesc_q = tc::idesc_bf16(128, HD, false, true);
       tc::mbar_wait(qo_full, 0);
       const uint32_t q_base = tc::smem_u32(sQ), do_base = tc::smem_u32(sdO);
-      for (int j = 0; j <= nblk; ++j) {
-        if (j < nblk) {
+      int sj = 0, gj = 0;  // polled issue queues: S/dP of block sj, dQ += dS K of block gj
+      while (gj < nblk) {
+        if (sj < nblk && tc::mbar_test(&kv_full[sj % KST], (sj / KST) & 1) &&
+            tc::mbar_test(&s_empty[sj & 1], ((sj >> 1) & 1) ^ 1)) {
+          const int j = sj++;
           const int b = j & 1, st = j % KST;
-          const uint32_t ph = (j >> 1) & 1;
-          tc::mbar_wait(&kv_full[st], (j / KST) & 1);
-          tc::mbar_wait(&s_empty[b], ph ^ 1);
           tc::tc_fence_after();
           const uint32_t k_base = tc::smem_u32(sK + st * K_T), v_base = tc::smem_u32(sV + st * K_T);
 #pragma unroll
@@ -665,11 +688,11 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ 
                             tc::smem_desc(v_base + off_k, 16, 1024, tc::kSwizzle128B), idesc_s, kk > 0);
           }
           tc::mma_commit(&s_full[b]);
+          continue;
         }
-        if (j >= 1) {
+        if (gj < sj && tc::mbar_test(&ds_full[gj & 1], (gj >> 1) & 1)) {
+          const int j = ++gj;  // j - 1 == the block being consumed (keeps the (j - 1) terms below)
           const int b = (j - 1) & 1, st = (j - 1) % KST;
-          const uint32_t ph = ((j - 1) >> 1) & 1;
-          tc::mbar_wait(&ds_full[b], ph);
           tc::tc_fence_after();
           const uint32_t ds = tc::smem_u32(sdS + b * DS_T), k_base = tc::smem_u32(sK + st * K_T);
 #pragma unroll
@@ -692,8 +715,8 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ 
     const bool valid = row < p.n;
     const int64_t qpos = p.q_off + row;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    const float lse2 = valid ? p.lse[static_cast<int64_t>(head) * p.n + row] * 1.4426950408889634f : 0.f;
-    const float dlt = valid ? p.delta[static_cast<int64_t>(head) * p.n + row] : 0.f;
+    const float2 ldv = *reinterpret_cast<const float2*>(p.ld + (static_cast<int64_t>(head) * p.n_pad + row) * 2);
+    const float lse2 = ldv.x, dlt = ldv.y;  // zero-padded past n
     for (int j = 0; j < nblk; ++j) {
       const int b = j & 1;
       const uint32_t ph = (j >> 1) & 1;
@@ -811,7 +834,29 @@ void attn_fwd_tc(const void* q, const void* kv, void* o, float* lse, int64_t n, 
   }
 }
 
-void attn_delta(DType t, const void* o, const void* dout, float* delta, int64_t n, int H, int hd, cudaStream_t s);
+namespace {
+// ld[head][i] = (lse * log2e, sum_d dO*O) for i < n, zeros up to n_pad: the
+// per-query vectors the backward kernels stream (one warp per (i, head)).
+__global__ void attn_prep_k(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                            const float* __restrict__ lse, float* __restrict__ ld, int64_t n, int64_t n_pad, int H,
+                            int hd) {
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (w >= n_pad * H) return;
+  const int head = static_cast<int>(w / n_pad);
+  const int64_t i = w % n_pad;
+  float d = 0.f, l = 0.f;
+  if (i < n) {
+    const int64_t base = i * (int64_t)H * hd + head * hd;
+    for (int c = lane; c < hd; c += 32) d += __bfloat162float(o[base + c]) * __bfloat162float(dout[base + c]);
+    d = warp_sum(d);
+    l = lse[(int64_t)head * n + i] * 1.4426950408889634f;
+  }
+  if (lane == 0) *reinterpret_cast<float2*>(ld + (head * n_pad + i) * 2) = make_float2(l, d);
+}
+}  // namespace
+
+size_t attn_bwd_ws_delta_floats(int64_t n, int H) { return static_cast<size_t>(H) * ((n + 63) / 64 * 64) * 2; }
 
 void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout, const float* lse, float* ws_delta,
                  float* ws_dq, void* dq, float* dkv, int64_t n, int64_t q_off, int64_t kv_len, int H, int hd,
@@ -820,14 +865,20 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kv) | reinterpret_cast<uintptr_t>(dout) |
        reinterpret_cast<uintptr_t>(dq) | reinterpret_cast<uintptr_t>(dkv)) & 15)
     throw std::invalid_argument("attention: operands must be 16-byte aligned");
-  attn_delta(DType::kBF16, o, dout, ws_delta, n, H, hd, s);
+  const int64_t n_pad = (n + 63) / 64 * 64;
+  {
+    const int64_t warps = n_pad * H;
+    attn_prep_k<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, ws_delta, n, n_pad, H, hd);
+    SPK_LAUNCH_CHECK();
+  }
   // dKV kernel: Q/dO boxes of 64 rows, KV boxes of 128 rows; dQ kernel: the reverse.
   AttnBwdParams a;
   make_map(&a.tq, q, h, n, h, 64);
   make_map(&a.tdo, dout, h, n, h, 64);
   make_map(&a.tkv, kv, 2 * h, kv_len, 2 * h, 128);
-  a.lse = lse;
-  a.delta = ws_delta;
+  a.ld = ws_delta;
+  a.n_pad = n_pad;
   a.dkv = dkv;
   a.dq = static_cast<__nv_bfloat16*>(dq);
   a.n = n;
@@ -837,6 +888,11 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
   a.h = h;
   a.scale = 1.f / sqrtf(static_cast<float>(hd));
   a.scale_log2 = 1.4426950408889634f * a.scale;
+  static const int dbg = [] {
+    const char* e = std::getenv("SP_ATTN_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dbg = dbg;
   AttnBwdParams b = a;
   make_map(&b.tq, q, h, n, h, 128);
   make_map(&b.tdo, dout, h, n, h, 128);
@@ -851,8 +907,22 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
     const size_t smem_dq = 2 * NC * CHUNK + 2 * KST * (NC * CHUNK / 2) + 2 * CHUNK + (6 + 2 * KST) * 8 + 8 + 1024;
     SPK_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dkv));
     SPK_CUDA(cudaFuncSetAttribute(attn_bwd_dq_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dq));
-    dim3 g1(static_cast<unsigned>((kv_len + 127) / 128), static_cast<unsigned>(H));
-    attn_bwd_dkv_k<HD><<<g1, 384, smem_dkv, s>>>(a);
+    {
+      const unsigned nkb2 = static_cast<unsigned>(((kv_len + 127) / 128 + 1) & ~int64_t(1));
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(nkb2, static_cast<unsigned>(H));
+      lc.blockDim = dim3(384);
+      lc.dynamicSmemBytes = smem_dkv;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      SPK_CUDA(cudaLaunchKernelEx(&lc, attn_bwd_dkv_k<HD>, a));
+    }
     SPK_LAUNCH_CHECK();
     dim3 g2(static_cast<unsigned>((n + 127) / 128), static_cast<unsigned>(H));
     attn_bwd_dq_k<HD><<<g2, 384, smem_dq, s>>>(b);
