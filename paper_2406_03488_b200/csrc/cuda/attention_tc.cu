@@ -1,23 +1,30 @@
-// tcgen05 causal prefix attention (bf16 in, fp32 softmax/accumulation).
+// tcgen05 causal prefix attention for Seq1F1B (bf16 in, fp32 softmax and
+// accumulation, sm_100a).
 //
-// Forward: one CTA per (128-query block, head) of sub-sequence s, streaming the
-// KV prefix [0, q_off + n) of the micro-batch's KV slab in 128-key blocks.
-//   warp 0     TMA: Q once; K_j / V_j into a 2-stage ring (one tensor map over
-//              the [kv_len, 2h] slab serves both: K at column head*hd, V at
-//              h + head*hd)
-//   warp 1     MMA: S_j = Q K_j^T (128x128xhd, SS) into TMEM S[j%2]; then
-//              O_{j-1} = P_{j-1} V_{j-1} (128 x hd x 128, A = P from SMEM,
-//              B = V as the MN-major operand) into TMEM O[(j-1)%2]
-//   warps 4-7  softmax, one query row per thread: tcgen05.ld S row, online
-//              max / exp2 / sum in fp32, P (bf16) written to SMEM in the
-//              canonical K-major SW128 layout; O_{j-1} read back from TMEM
-//              and rescaled into registers while the tensor core already
-//              works on S_{j+1} / O_j.
-// TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).
+// A sub-sequence s of n queries (global positions q_off..q_off+n-1) attends to
+// the micro-batch's KV-prefix slab rows [0, q_off + n): the causal edge
+// F(m,s-1) -> F(m,s) of the reference dependency model
+// (/root/reference/proj/core/src/sim.cpp:24-27). The backward adds dK/dV for
+// those rows into the stage's fp32 accumulator (reverse edge, sim.cpp:34-36).
+//
+// Head-dim tiling. A [rows x hd] bf16 tile is stored as a 64-column chunk in
+// the canonical 128-byte-swizzled layout plus, for hd > 64, a second chunk:
+// hd 128 -> another 64-column SW128 chunk; hd 80 -> a 16-column chunk in the
+// 32-byte-swizzled layout (no padding: 160 B per row instead of 256 B). A tile
+// serves both as a K-major operand (rows = M/N) and, unchanged, as an MN-major
+// operand (rows = K); MN-major GEMMs with N = hd 80 issue an N=64 and an N=16
+// MMA into adjacent TMEM columns.
+//
+// Forward: one CTA per (128 queries, head). warp 0 = TMA (Q once, K/V rings, K
+// running one block ahead of V), warp 1 = MMA issuer polling two queues (S_j =
+// Q K_j^T and O += P_j V_j), warps 4-7 = softmax (one query row per thread, S
+// row in registers, P to SMEM, O accumulated in TMEM with lazy rescaling).
+// Backward: dK/dV kernel (2-CTA clusters of 128-key blocks, Q/dO tiles
+// multicast to both CTAs, 8 softmax warps) and dQ kernel (128-query blocks);
+// both deterministic, no atomics.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
-#include <mutex>
 
 #include "cuda/common.cuh"
 #include "cuda/ops.h"
@@ -30,19 +37,96 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn();  // gemm_tcgen05.cu
 namespace {
 
 constexpr int BQ = 128, BKV = 128;
-constexpr int CHUNK = 128 * 128;  // bytes of one [128 rows x 64 bf16] SW128 chunk
+
+#ifndef SPK_ATTN_NARROW80
+#define SPK_ATTN_NARROW80 0  // measured slower on B200 (extra N=16 MMAs, 32-byte TMA rows)
+#endif
+
+template <int HD>
+struct Lay {
+  static constexpr bool NARROW = HD == 80 && SPK_ATTN_NARROW80;  // hd 80: SW32 16-column second chunk
+  static constexpr int C1 = HD <= 64 ? 0 : (NARROW ? 16 : 64);  // columns held by the second chunk
+  static constexpr int R1 = C1 * 2;                              // bytes per row of the second chunk
+  static constexpr int bytes(int rows) { return rows * (128 + R1); }
+};
+
+// K-major descriptor of head-dim step kk (16 dims) of a [rows x hd] tile.
+template <int HD>
+__device__ __forceinline__ uint64_t kdesc(uint32_t base, int rows, int kk) {
+  if (kk < 4) return tc::smem_desc(base + kk * 32, 16, 1024, tc::kSwizzle128B);
+  if constexpr (Lay<HD>::NARROW) {
+    return tc::smem_desc(base + rows * 128, 16, 256, tc::kSwizzle32B);
+  } else {
+    return tc::smem_desc(base + rows * 128 + (kk - 4) * 32, 16, 1024, tc::kSwizzle128B);
+  }
+}
+
+// D[128 x hd] (+)= A[128 x 16 (K step kk)] * B[K rows of a [rows x hd] tile]^T, B MN-major.
+template <int HD>
+__device__ __forceinline__ void mma_nhd(uint32_t d, uint64_t adesc, uint32_t bbase, int rows, int kk, bool acc) {
+  if constexpr (Lay<HD>::NARROW) {
+    constexpr uint32_t i64 = tc::idesc_bf16(128, 64, false, true), i16 = tc::idesc_bf16(128, 16, false, true);
+    tc::mma_bf16_ss(d, adesc, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), i64, acc);
+    tc::mma_bf16_ss(d + 64, adesc, tc::smem_desc(bbase + rows * 128 + kk * 512, 256, 256, tc::kSwizzle32B), i16, acc);
+  } else {  // padded second chunk: one N = hd MMA
+    constexpr uint32_t id = tc::idesc_bf16(128, HD, false, true);
+    tc::mma_bf16_ss(d, adesc, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), id, acc);
+  }
+}
+
+// Same with A (M=128 x K=16, bf16 packed two per 32-bit column) read from TMEM.
+template <int HD>
+__device__ __forceinline__ void mma_nhd_ts(uint32_t d, uint32_t a_tmem, uint32_t bbase, int rows, int kk, bool acc) {
+  if constexpr (Lay<HD>::NARROW) {
+    constexpr uint32_t i64 = tc::idesc_bf16(128, 64, false, true), i16 = tc::idesc_bf16(128, 16, false, true);
+    tc::mma_bf16_ts(d, a_tmem, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), i64, acc);
+    tc::mma_bf16_ts(d + 64, a_tmem, tc::smem_desc(bbase + rows * 128 + kk * 512, 256, 256, tc::kSwizzle32B), i16, acc);
+  } else {
+    constexpr uint32_t id = tc::idesc_bf16(128, HD, false, true);
+    tc::mma_bf16_ts(d, a_tmem, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), id, acc);
+  }
+}
+
+// TMEM column of K-step kk (16 columns of a 64-wide bf16 operand) when each
+// half (32 columns) of the operand was packed at the start of its own 32
+// fp32 columns (the softmax half that produced it overwrites only its slice).
+__device__ __forceinline__ uint32_t half_packed_col(int kk) { return 32 * (kk >> 1) + 8 * (kk & 1); }
+
+__device__ __forceinline__ float4 lds_f4(const void* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
+struct Maps {  // chunk-0 and chunk-1 tensor maps of one [rows, cols] bf16 tensor
+  CUtensorMap m0, m1;
+};
+
+// TMA a [rows x hd] tile at (col, row) of the tensor into dst (both chunks).
+template <int HD>
+__device__ __forceinline__ void load_tile(uint8_t* dst, const Maps& t, uint64_t* bar, int col, int row, int rows,
+                                          uint16_t mc) {
+  if (mc) {
+    tc::tma_load_2d_mc(dst, &t.m0, bar, col, row, mc);
+    if constexpr (HD > 64) tc::tma_load_2d_mc(dst + rows * 128, &t.m1, bar, col + 64, row, mc);
+  } else {
+    tc::tma_load_2d(dst, &t.m0, bar, col, row);
+    if constexpr (HD > 64) tc::tma_load_2d(dst + rows * 128, &t.m1, bar, col + 64, row);
+  }
+}
 
 struct __align__(64) AttnParams {
-  CUtensorMap tq;   // q [n, h]
-  CUtensorMap tkv;  // kv [kv_len, 2h]
+  Maps tq;   // q [n, h], 128-row boxes
+  Maps tkv;  // kv [kv_len, 2h], 128-row boxes
   __nv_bfloat16* o;
   float* lse;
   int64_t n, q_off, kv_len;
-  int H, hd, h;
+  int H, h;
   float scale_log2;
 };
 
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
@@ -51,17 +135,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
-}
-
-// Store 32 bf16 values (16 packed words) of row r, columns [c32*32, c32*32+32) of a
-// K-major SW128 [128 x 128] tile made of two 64-column chunks.
-__device__ __forceinline__ void st_tile_row32(uint8_t* tile, int r, int c32, const uint32_t (&w)[16]) {
-  uint8_t* chunk = tile + (c32 >> 1) * CHUNK + r * 128;
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int unit = ((c32 & 1) * 4 + u) ^ (r & 7);
-    *reinterpret_cast<uint4*>(chunk + unit * 16) = make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
-  }
 }
 
 // One MUFU.EX2 (exp2f() adds range-reduction FMUL/FSETP/FSEL around it).
@@ -77,27 +150,42 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 }
 
 template <int HD>
+constexpr size_t fwd_smem_n(int st) {
+  return Lay<HD>::bytes(128) * (1 + 2 * st) + (10 + 4 * st) * 8 + 8 + 1024;
+}
+// Ring depths: as many stages as the opt-in SMEM (227 KB) holds, capped at 4 / 6 / 8.
+template <int HD>
+constexpr int fwd_stages() {
+  int st = 4;
+  while (fwd_smem_n<HD>(st) > 232448) --st;
+  return st;
+}
+template <int HD>
+constexpr size_t fwd_smem() {
+  return fwd_smem_n<HD>(fwd_stages<HD>());
+}
+
+// ============================================================================ forward
+
+template <int HD>
 __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ AttnParams p) {
-  constexpr int NC = (HD + 63) / 64;  // 64-wide K chunks of the head dim
-  constexpr int QBYTES = NC * CHUNK, KBYTES = NC * CHUNK, VBYTES = NC * CHUNK, PBYTES = 2 * CHUNK;
+  constexpr int KVS = fwd_stages<HD>();
+  constexpr int TB = Lay<HD>::bytes(128);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = sm;
-  uint8_t* sK = sQ + QBYTES;          // [2][KBYTES]
-  uint8_t* sV = sK + 2 * KBYTES;      // [2][VBYTES]
-  uint8_t* sP = sV + 2 * VBYTES;      // [2][PBYTES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * PBYTES);
+  uint8_t* sK = sQ + TB;           // [KVS]
+  uint8_t* sV = sK + KVS * TB;     // [KVS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + KVS * TB);
   uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* v_full = bars + 3;   // [2]
-  uint64_t* kv_empty = bars + 5; // [2]
-  uint64_t* s_full = bars + 7;   // [2]
-  uint64_t* s_empty = bars + 9;  // [2]
-  uint64_t* p_full = bars + 11;  // [2]
-  uint64_t* p_empty = bars + 13; // [2]
-  uint64_t* o_done = bars + 15;  // one phase per PV MMA group
-  uint64_t* v_empty = bars + 16; // [2]  (kv_empty above now releases K stages only)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
+  uint64_t* s_full = bars + 1;   // [2]
+  uint64_t* p_full = bars + 5;   // [2]
+  uint64_t* p_empty = bars + 7;  // [2]
+  uint64_t* k_full = bars + 10;          // [KVS]
+  uint64_t* k_empty = k_full + KVS;      // [KVS]
+  uint64_t* v_full = k_empty + KVS;      // [KVS]
+  uint64_t* v_empty = v_full + KVS;      // [KVS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + KVS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int num_qb = static_cast<int>((p.n + BQ - 1) / BQ);
@@ -111,16 +199,16 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
   if (threadIdx.x == 0) {
     tc::mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&k_full[i], 1);
-      tc::mbar_init(&v_full[i], 1);
-      tc::mbar_init(&kv_empty[i], 1);
-      tc::mbar_init(&v_empty[i], 1);
       tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&s_empty[i], 128);
       tc::mbar_init(&p_full[i], 128);
       tc::mbar_init(&p_empty[i], 1);
     }
-    tc::mbar_init(o_done, 1);
+    for (int i = 0; i < KVS; ++i) {
+      tc::mbar_init(&k_full[i], 1);
+      tc::mbar_init(&k_empty[i], 1);
+      tc::mbar_init(&v_full[i], 1);
+      tc::mbar_init(&v_empty[i], 1);
+    }
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -128,80 +216,70 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // TMEM: S0 [0,128) S1 [128,256) O [256, 256+hd). P_j (bf16) overwrites the
+  // first 64 columns of its S buffer and feeds the PV MMA straight from TMEM.
 
   if (warp == 0) {
     if (lane == 0) {
-      tc::tma_prefetch(&p.tq);
-      tc::tma_prefetch(&p.tkv);
-      tc::mbar_expect_tx(q_full, QBYTES);
-      for (int c = 0; c < NC; ++c)
-        tc::tma_load_2d(sQ + c * CHUNK, &p.tq, q_full, head * HD + 64 * c, static_cast<int>(q0));
-      // K runs one block ahead of V: K_{j+1} (freed after S_{j-1}) is requested
-      // before V_j (freed after PV_{j-2}) so a slow PV never starves S.
+      tc::tma_prefetch(&p.tq.m0);
+      tc::tma_prefetch(&p.tkv.m0);
+      tc::mbar_expect_tx(q_full, TB);
+      load_tile<HD>(sQ, p.tq, q_full, head * HD, static_cast<int>(q0), 128, 0);
+      // K runs one block ahead of V: K_{j+1} (freed after S_{j+1-KVS}) is
+      // requested before V_j (freed after PV_{j-KVS}), so PV never starves S.
       auto load_k = [&](int j) {
-        const int st = j & 1;
-        tc::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        tc::mbar_expect_tx(&k_full[st], KBYTES);
-        for (int c = 0; c < NC; ++c)
-          tc::tma_load_2d(sK + st * KBYTES + c * CHUNK, &p.tkv, &k_full[st], head * HD + 64 * c, j * BKV);
+        const int st = j % KVS;
+        tc::mbar_wait(&k_empty[st], ((j / KVS) & 1) ^ 1);
+        tc::mbar_expect_tx(&k_full[st], TB);
+        load_tile<HD>(sK + st * TB, p.tkv, &k_full[st], head * HD, j * BKV, 128, 0);
       };
       if (nblk > 0) load_k(0);
       for (int j = 0; j < nblk; ++j) {
         if (j + 1 < nblk) load_k(j + 1);
-        const int st = j & 1;
-        tc::mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
-        tc::mbar_expect_tx(&v_full[st], VBYTES);
-        for (int c = 0; c < NC; ++c)
-          tc::tma_load_2d(sV + st * VBYTES + c * CHUNK, &p.tkv, &v_full[st], p.h + head * HD + 64 * c, j * BKV);
+        const int st = j % KVS;
+        tc::mbar_wait(&v_empty[st], ((j / KVS) & 1) ^ 1);
+        tc::mbar_expect_tx(&v_full[st], TB);
+        load_tile<HD>(sV + st * TB, p.tkv, &v_full[st], p.h + head * HD, j * BKV, 128, 0);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc_s = tc::idesc_bf16(128, BKV, false, false);
-      constexpr uint32_t idesc_o = tc::idesc_bf16(128, HD, false, true);
       tc::mbar_wait(q_full, 0);
       const uint32_t q_base = tc::smem_u32(sQ);
-      // Poll two queues: S_j (needs K_j and a free S buffer) and PV_j (needs P_j
-      // and V_j). K and V stages are released separately (K after S_j, V after
-      // PV_j), so S can run two blocks ahead of the softmax.
+      // Poll two queues: S_j (needs K_j, and PV_{j-2} issued: S_j overwrites
+      // the buffer P_{j-2} is read from; MMAs execute in issue order) and PV_j
+      // (needs P_j and V_j).
       int sj = 0, pj = 0;
       while (pj < nblk) {
-        if (sj < nblk && tc::mbar_test(&k_full[sj & 1], (sj >> 1) & 1) &&
-            tc::mbar_test(&s_empty[sj & 1], ((sj >> 1) & 1) ^ 1)) {
-          const int b = sj & 1;
+        if (sj < nblk && sj < pj + 2 && tc::mbar_test(&k_full[sj % KVS], (sj / KVS) & 1)) {
+          const int b = sj & 1, st = sj % KVS;
           tc::tc_fence_after();
-          const uint32_t k_base = tc::smem_u32(sK + b * KBYTES);
+          const uint32_t k_base = tc::smem_u32(sK + st * TB);
 #pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * CHUNK + (kk & 3) * 32;
-            tc::mma_bf16_ss(tmem + b * 128, tc::smem_desc(q_base + off, 16, 1024, tc::kSwizzle128B),
-                            tc::smem_desc(k_base + off, 16, 1024, tc::kSwizzle128B), idesc_s, kk > 0);
-          }
+          for (int kk = 0; kk < HD / 16; ++kk)
+            tc::mma_bf16_ss(tmem + b * 128, kdesc<HD>(q_base, 128, kk), kdesc<HD>(k_base, 128, kk), idesc_s, kk > 0);
           tc::mma_commit(&s_full[b]);
-          tc::mma_commit(&kv_empty[b]);  // K stage free
+          tc::mma_commit(&k_empty[st]);
           ++sj;
           continue;
         }
-        if (pj < sj && tc::mbar_test(&p_full[pj & 1], (pj >> 1) & 1) && tc::mbar_test(&v_full[pj & 1], (pj >> 1) & 1)) {
-          const int b = pj & 1;
+        if (pj < sj && tc::mbar_test(&p_full[pj & 1], (pj >> 1) & 1) &&
+            tc::mbar_test(&v_full[pj % KVS], (pj / KVS) & 1)) {
+          const int b = pj & 1, st = pj % KVS;
           tc::tc_fence_after();
-          const uint32_t p_base = tc::smem_u32(sP + b * PBYTES);
-          const uint32_t v_base = tc::smem_u32(sV + b * VBYTES);
+          const uint32_t v_base = tc::smem_u32(sV + st * TB);
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk) {
-            const uint64_t ad = tc::smem_desc(p_base + (kk >> 2) * CHUNK + (kk & 3) * 32, 16, 1024, tc::kSwizzle128B);
-            const uint64_t bd = tc::smem_desc(v_base + kk * 2048, CHUNK, 1024, tc::kSwizzle128B);
-            tc::mma_bf16_ss(tmem + 256, ad, bd, idesc_o, pj > 0 || kk > 0);  // O accumulates in TMEM
-          }
-          tc::mma_commit(o_done);
-          tc::mma_commit(&p_empty[b]);
-          tc::mma_commit(&v_empty[b]);  // V stage free
+          for (int kk = 0; kk < BKV / 16; ++kk)  // O accumulates in TMEM; A = P_j from TMEM
+            mma_nhd_ts<HD>(tmem + 256, tmem + b * 128 + kk * 8, v_base, 128, kk, pj > 0 || kk > 0);
+          tc::mma_commit(&p_empty[b]);  // also marks PV_pj (and every earlier MMA) complete
+          tc::mma_commit(&v_empty[st]);
           ++pj;
         }
       }
     }
   } else if (warp >= 4) {
-    // Softmax: S row in registers (one pass), P -> SMEM, O stays in TMEM. The
+    // Softmax: S row in registers (one pass), P -> TMEM, O stays in TMEM. The
     // running max used for exponentiation only moves when a block raises it by
     // more than 2^8 (log2 domain); then the O row in TMEM is rescaled once
     // PV_{j-1} has landed. Otherwise the softmax never waits for the PV MMAs.
@@ -227,8 +305,6 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
 #pragma unroll
       for (int c = 0; c < 4; ++c) tc::tmem_ld32(sbase + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
       tc::tmem_ld_wait();
-      tc::tc_fence_before();
-      tc::mbar_arrive(&s_empty[b]);  // S buffer free: the MMA warp may issue S_{j+2}
       // Raw scores stay unscaled (scale > 0 commutes with max); masking only on
       // blocks that touch the causal diagonal or the prefix end.
       float mx = -INFINITY;
@@ -248,7 +324,10 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
         const float m_new = need ? fmaxf(m, mx) : m;
         const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
         if (j > 0) {  // rescale the O row accumulated so far (PV_{j-1} must have landed)
-          tc::mbar_wait(o_done, (j - 1) & 1);
+          // PV_{j-1} landed <=> phase (j-1)>>1 of p_empty[(j-1)&1] completed. The
+          // softmax already waited for that buffer's previous phase, so the
+          // parity wait cannot alias an older phase.
+          tc::mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
           tc::tc_fence_after();
 #pragma unroll
           for (int c = 0; c < HD / 16; ++c) {
@@ -265,8 +344,6 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
         m = m_new;
       }
       const float neg_m = m == -INFINITY ? 0.f : -m;
-      tc::mbar_wait(&p_empty[b], ph ^ 1);
-      uint8_t* ptile = sP + b * PBYTES;
       float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -279,15 +356,14 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
           rs1 += p1;
           w[e / 2] = pack_bf16(p0, p1);
         }
-        st_tile_row32(ptile, r, c, w);
+        tc::tmem_st16(sbase + c * 16, w);  // P keys [32c, 32c+32) -> columns [16c, 16c+16)
       }
-      const float rs = rs0 + rs1;
-      l += rs;
+      l += rs0 + rs1;
+      tc::tmem_st_wait();
       tc::tc_fence_before();
-      fence_async_smem();
       tc::mbar_arrive(&p_full[b]);
     }
-    tc::mbar_wait(o_done, (nblk - 1) & 1);  // last PV landed
+    if (nblk > 0) tc::mbar_wait(&p_empty[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);  // last PV landed
     tc::tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     __nv_bfloat16* orow = p.o + (valid ? row : 0) * p.h + head * HD;
@@ -317,56 +393,71 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
 }
 
 // ============================================================================ backward
-//
-// dK/dV kernel: one CTA per (128-key block, head), looping over 64-query
-// blocks that can see those keys:
-//   S^T = K Q_i^T, dP^T = V dO_i^T (M = 128 keys, N = 64 queries) into TMEM;
-//   one thread per key row: P^T = exp2(S^T*c - LSE), dS^T = P^T (dP^T - D)
-//   written to SMEM (K-major); dV += P^T dO_i and dK += dS^T Q_i accumulate in
-//   TMEM (the Q_i / dO_i tiles double as MN-major B operands: a [rows x 64]
-//   SW128 tile is both layouts). The block's dK/dV are added once into the fp32
-//   dKV accumulator: each (key row, head) slice has one owner (no atomics).
-// dQ kernel: one CTA per (128-query block, head), looping over 64-key blocks:
-//   S = Q K_j^T, dP = dO V_j^T; dS = P (dP - D) -> SMEM; dQ += dS K_j in TMEM.
-// Together: 7 tensor-core GEMMs per (q,k) block pair, fully deterministic.
 
 struct __align__(64) AttnBwdParams {
-  CUtensorMap tq;    // q   [n, h]      box 64 rows
-  CUtensorMap tdo;   // dO  [n, h]      box 64 rows (dKV kernel) / 128 rows (dQ kernel)
-  CUtensorMap tkv;   // kv  [kv_len, 2h] box 128 rows (dKV kernel) / 64 rows (dQ kernel)
-  const float* ld;     // [H, n_pad] x (LSE * log2e, delta), zero padded (attn_prep_k)
-  int64_t n_pad;       // n rounded up to 64
+  Maps tq;           // q  [n, h]
+  Maps tdo;          // dO [n, h]
+  Maps tkv;          // kv [kv_len, 2h]
+  const float* ld;   // [H, n_pad] x (LSE * log2e, delta), zero padded (attn_prep_k)
+  int64_t n_pad;     // n rounded up to 64
   float* dkv;        // [kv_len, 2h] fp32 accumulator
   __nv_bfloat16* dq; // [n, h]
   int64_t n, q_off, kv_len;
   int H, h;
   float scale, scale_log2;
-  int dbg;  // profiling only (SP_ATTN_DBG): 1 = skip MMAs, 2 = skip softmax math
+  int dbg;  // profiling only (SP_ATTN_DBG): 1 = skip dK/dV MMAs, 2 = skip dK/dV softmax math
 };
 
 template <int HD>
+constexpr size_t dkv_smem_n(int st) {
+  return 2 * Lay<HD>::bytes(128) + 2 * st * Lay<HD>::bytes(64) + st * 512 + (10 + 2 * st) * 8 + 8 + 1024;
+}
+template <int HD>
+constexpr int dkv_stages() {
+  int st = 6;
+  while (dkv_smem_n<HD>(st) > 232448) --st;
+  return st;
+}
+template <int HD>
+constexpr size_t dkv_smem() {
+  return dkv_smem_n<HD>(dkv_stages<HD>());
+}
+template <int HD>
+constexpr size_t dq_smem_n(int st) {
+  return 2 * Lay<HD>::bytes(128) + 2 * st * Lay<HD>::bytes(64) + (10 + 2 * st) * 8 + 8 + 1024;
+}
+template <int HD>
+constexpr int dq_stages() {
+  int st = 8;
+  while (dq_smem_n<HD>(st) > 232448) --st;
+  return st;
+}
+template <int HD>
+constexpr size_t dq_smem() {
+  return dq_smem_n<HD>(dq_stages<HD>());
+}
+
+// dK/dV: one CTA per (128-key block, head), looping over 64-query blocks that
+// can see those keys: S^T = K Q_i^T and dP^T = V dO_i^T into TMEM; the softmax
+// warps form P^T = exp2(S^T*c - LSE) and dS^T = P^T (dP^T - delta) as bf16
+// over their S^T / dP^T columns in TMEM; dV += P^T dO_i and dK += dS^T Q_i
+// take A from TMEM and accumulate in TMEM. Each (key row, head) slice of the
+// fp32 dKV accumulator has exactly one owner CTA.
+template <int HD>
 __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__ AttnBwdParams p) {
-  constexpr int NC = (HD + 63) / 64;
-  constexpr int KV_T = NC * CHUNK;       // [128 rows x hd] tile
-  constexpr int Q_T = NC * CHUNK / 2;    // [64 rows x hd] tile (chunks of 8 KB)
-  constexpr int QCH = CHUNK / 2;
-  constexpr int PT = CHUNK;              // [128 keys x 64 queries] bf16 tile
-  constexpr int QST = NC == 1 ? 4 : 3;   // Q / dO / (LSE, delta) ring depth
+  constexpr int QST = dkv_stages<HD>();
+  constexpr int KV_T = Lay<HD>::bytes(128), Q_T = Lay<HD>::bytes(64);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = sm;
   uint8_t* sV = sK + KV_T;
   uint8_t* sQ = sV + KV_T;          // [QST]
   uint8_t* sdO = sQ + QST * Q_T;    // [QST]
-  uint8_t* sPt = sdO + QST * Q_T;   // [2]
-  uint8_t* sdSt = sPt + 2 * PT;     // [2]
-  float* sLD = reinterpret_cast<float*>(sdSt + 2 * PT);  // [QST][64 x (lse*log2e, delta)]
+  float* sLD = reinterpret_cast<float*>(sdO + QST * Q_T);  // [QST][64 x (lse*log2e, delta)]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + QST * 128);
   uint64_t* kv_full = bars;
   uint64_t* s_full = bars + 1;   // [2]
-  uint64_t* s_empty = bars + 3;  // [2]
   uint64_t* p_full = bars + 5;   // [2]
-  uint64_t* p_empty = bars + 7;  // [2]
   uint64_t* done = bars + 9;
   uint64_t* q_full = bars + 10;          // [QST]
   uint64_t* q_empty = q_full + QST;      // [QST]
@@ -374,12 +465,12 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
 
   // 2-CTA cluster: CTAs own adjacent 128-key blocks and stream the same query
   // blocks; each Q_i / dO_i tile is fetched once from L2 and multicast to both
-  // (rank 0 issues Q, rank 1 issues dO), halving the dominant L2 -> SMEM traffic.
+  // (rank 0 issues Q, rank 1 issues dO).
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = tc::cluster_ctarank();
   const int num_kb = static_cast<int>((p.kv_len + 127) / 128);
   const int num_kb2 = (num_kb + 1) & ~1;
-  const int kb = num_kb2 - 1 - static_cast<int>(blockIdx.x);   // heaviest first; may be == num_kb (idle keys)
+  const int kb = num_kb2 - 1 - static_cast<int>(blockIdx.x);  // heaviest first; may be == num_kb (idle keys)
   const int head = blockIdx.y;
   const int64_t j0 = static_cast<int64_t>(kb) * 128;
   const int64_t j0_lo = static_cast<int64_t>(num_kb2 - 2 - 2 * static_cast<int>(blockIdx.x / 2)) * 128;
@@ -393,9 +484,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
     tc::mbar_init(done, 1);
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&s_empty[i], 256);
       tc::mbar_init(&p_full[i], 256);
-      tc::mbar_init(&p_empty[i], 1);
     }
     for (int i = 0; i < QST; ++i) {
       tc::mbar_init(&q_full[i], 1);
@@ -408,34 +497,26 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
   tc::cluster_sync();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: S^T[2] at 0/64, dP^T[2] at 128/192, dV at 256, dK at 384.
+  // TMEM: S^T[2] at 0/64, dP^T[2] at 128/192, dV at 256, dK at 384. P^T and
+  // dS^T (bf16) overwrite the S^T / dP^T columns they were computed from.
 
   if (warp == 0) {
-    // Producer warp: K/V once; per query block the Q / dO tiles (TMA) and the
-    // block's LSE / delta vectors (all 32 lanes), QST stages ahead of the consumers.
     if (lane == 0) {
-      tc::tma_prefetch(&p.tq);
-      tc::tma_prefetch(&p.tdo);
-      tc::tma_prefetch(&p.tkv);
+      tc::tma_prefetch(&p.tq.m0);
+      tc::tma_prefetch(&p.tdo.m0);
+      tc::tma_prefetch(&p.tkv.m0);
       tc::mbar_expect_tx(kv_full, 2 * KV_T);
-      for (int c = 0; c < NC; ++c) {
-        tc::tma_load_2d(sK + c * CHUNK, &p.tkv, kv_full, head * HD + 64 * c, static_cast<int>(j0));
-        tc::tma_load_2d(sV + c * CHUNK, &p.tkv, kv_full, p.h + head * HD + 64 * c, static_cast<int>(j0));
-      }
-    }
-    if (lane == 0) {
+      load_tile<HD>(sK, p.tkv, kv_full, head * HD, static_cast<int>(j0), 128, 0);
+      load_tile<HD>(sV, p.tkv, kv_full, p.h + head * HD, static_cast<int>(j0), 128, 0);
       for (int it = 0; it < niter; ++it) {
         const int st = it % QST;
         const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
         tc::mbar_wait(&q_empty[st], ((it / QST) & 1) ^ 1);  // stage free in both CTAs
         tc::mbar_expect_tx(&q_full[st], 2 * Q_T + 512);
-        for (int c = 0; c < NC; ++c) {
-          if (rank == 0)
-            tc::tma_load_2d_mc(sQ + st * Q_T + c * QCH, &p.tq, &q_full[st], head * HD + 64 * c, static_cast<int>(i0), 3);
-          else
-            tc::tma_load_2d_mc(sdO + st * Q_T + c * QCH, &p.tdo, &q_full[st], head * HD + 64 * c, static_cast<int>(i0),
-                               3);
-        }
+        if (rank == 0)
+          load_tile<HD>(sQ + st * Q_T, p.tq, &q_full[st], head * HD, static_cast<int>(i0), 64, 3);
+        else
+          load_tile<HD>(sdO + st * Q_T, p.tdo, &q_full[st], head * HD, static_cast<int>(i0), 64, 3);
         // (LSE*log2e, delta) pairs of the 64 queries: one async 512-byte bulk copy
         tc::bulk_load(sLD + st * 128, p.ld + (static_cast<int64_t>(head) * p.n_pad + i0) * 2, 512, &q_full[st]);
       }
@@ -443,19 +524,14 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc_s = tc::idesc_bf16(128, 64, false, false);
-      constexpr uint32_t idesc_g = tc::idesc_bf16(128, HD, false, true);
       tc::mbar_wait(kv_full, 0);
       const uint32_t k_base = tc::smem_u32(sK), v_base = tc::smem_u32(sV);
       // Two independent issue queues polled without blocking: S^T/dP^T of block
-      // s_it (needs its Q/dO stage and a free S buffer — released by the softmax
-      // warps right after their TMEM load) and dV/dK of block g_it (needs that
-      // block's P^T/dS^T). S can therefore run up to two blocks ahead of the
-      // softmax instead of waiting behind the previous dV/dK in program order.
+      // s_it (once dV/dK of block s_it-2, which read its TMEM buffer, have been
+      // issued: MMAs execute in issue order) and dV/dK of block g_it.
       int s_it = 0, g_it = 0;
       while (g_it < niter) {
-        const bool s_ready = s_it < niter && tc::mbar_test(&q_full[s_it % QST], (s_it / QST) & 1) &&
-                             tc::mbar_test(&s_empty[s_it & 1], ((s_it >> 1) & 1) ^ 1);
-        if (s_ready) {
+        if (s_it < niter && s_it < g_it + 2 && tc::mbar_test(&q_full[s_it % QST], (s_it / QST) & 1)) {
           const int it = s_it++;
           const int b = it & 1, st = it % QST;
           tc::tc_fence_after();
@@ -463,12 +539,9 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
           if (!(p.dbg & 1)) {
 #pragma unroll
             for (int kk = 0; kk < HD / 16; ++kk) {
-              const uint32_t off_kv = (kk >> 2) * CHUNK + (kk & 3) * 32;
-              const uint32_t off_q = (kk >> 2) * QCH + (kk & 3) * 32;
-              tc::mma_bf16_ss(tmem + b * 64, tc::smem_desc(k_base + off_kv, 16, 1024, tc::kSwizzle128B),
-                              tc::smem_desc(q_base + off_q, 16, 1024, tc::kSwizzle128B), idesc_s, kk > 0);
-              tc::mma_bf16_ss(tmem + 128 + b * 64, tc::smem_desc(v_base + off_kv, 16, 1024, tc::kSwizzle128B),
-                              tc::smem_desc(do_base + off_q, 16, 1024, tc::kSwizzle128B), idesc_s, kk > 0);
+              tc::mma_bf16_ss(tmem + b * 64, kdesc<HD>(k_base, 128, kk), kdesc<HD>(q_base, 64, kk), idesc_s, kk > 0);
+              tc::mma_bf16_ss(tmem + 128 + b * 64, kdesc<HD>(v_base, 128, kk), kdesc<HD>(do_base, 64, kk), idesc_s,
+                              kk > 0);
             }
           }
           tc::mma_commit(&s_full[b]);
@@ -478,18 +551,15 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
           const int it = g_it++;
           const int b = it & 1, st = it % QST;
           tc::tc_fence_after();
-          const uint32_t pt = tc::smem_u32(sPt + b * PT), dst = tc::smem_u32(sdSt + b * PT);
           const uint32_t q_base = tc::smem_u32(sQ + st * Q_T), do_base = tc::smem_u32(sdO + st * Q_T);
+          if (!(p.dbg & 1)) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries
-            if (p.dbg & 1) break;
-            const bool acc = it > 0 || kk > 0;
-            tc::mma_bf16_ss(tmem + 256, tc::smem_desc(pt + kk * 32, 16, 1024, tc::kSwizzle128B),
-                            tc::smem_desc(do_base + kk * 2048, QCH, 1024, tc::kSwizzle128B), idesc_g, acc);
-            tc::mma_bf16_ss(tmem + 384, tc::smem_desc(dst + kk * 32, 16, 1024, tc::kSwizzle128B),
-                            tc::smem_desc(q_base + kk * 2048, QCH, 1024, tc::kSwizzle128B), idesc_g, acc);
+            for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries
+              const bool acc = it > 0 || kk > 0;
+              mma_nhd_ts<HD>(tmem + 256, tmem + b * 64 + half_packed_col(kk), do_base, 64, kk, acc);
+              mma_nhd_ts<HD>(tmem + 384, tmem + 128 + b * 64 + half_packed_col(kk), q_base, 64, kk, acc);
+            }
           }
-          tc::mma_commit(&p_empty[b]);
           tc::mma_commit_mc(&q_empty[st], 3);  // this CTA is done with the multicast stage
         }
       }
@@ -507,7 +577,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
       const uint32_t ph = (it >> 1) & 1;
       const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
       const float* ld = sLD + st * 128 + half * 64;  // this half's 32 (lse, delta) pairs
-      tc::mbar_wait(&q_full[st], (it / QST) & 1);  // LSE / delta of this block are in SMEM
+      tc::mbar_wait(&q_full[st], (it / QST) & 1);    // LSE / delta of this block are in SMEM
       // visible query columns c (local to this half): q_off + i0 + 32*half + c >= kpos, i0 + 32*half + c < n
       const int64_t cbase = i0 + half * 32;
       int64_t cmin = kpos - p.q_off - cbase;
@@ -520,16 +590,13 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
       tc::tmem_ld32(tmem + lane_base + b * 64 + half * 32, sv);
       tc::tmem_ld32(tmem + lane_base + 128 + b * 64 + half * 32, dpv);
       tc::tmem_ld_wait();
-      tc::tc_fence_before();
-      tc::mbar_arrive(&s_empty[b]);
-      tc::mbar_wait(&p_empty[b], ph ^ 1);
       const bool full_blk = __all_sync(0xffffffffu, c_lo == 0 && c_hi == 32);
       uint32_t wp[16], wd[16];
 #pragma unroll
       for (int e = 0; e < 32; e += 4) {
         if (p.dbg & 2) break;
-        const float4 a4 = *reinterpret_cast<const float4*>(ld + 2 * e);      // (lse, delta) of queries e, e+1
-        const float4 b4 = *reinterpret_cast<const float4*>(ld + 2 * e + 4);  // (lse, delta) of queries e+2, e+3
+        const float4 a4 = lds_f4(ld + 2 * e);      // (lse, delta) of queries e, e+1 (warp broadcast)
+        const float4 b4 = lds_f4(ld + 2 * e + 4);  // (lse, delta) of queries e+2, e+3
         const float lv[4] = {a4.x, a4.z, b4.x, b4.z}, dl[4] = {a4.y, a4.w, b4.y, b4.w};
         float pv[4], dv[4];
 #pragma unroll
@@ -545,9 +612,10 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
         wd[e / 2] = pack_bf16(dv[0], dv[1]);
         wd[e / 2 + 1] = pack_bf16(dv[2], dv[3]);
       }
-      st_tile_row32(sPt + b * PT, r, half, wp);
-      st_tile_row32(sdSt + b * PT, r, half, wd);
-      fence_async_smem();
+      tc::tmem_st16(tmem + lane_base + b * 64 + half * 32, wp);
+      tc::tmem_st16(tmem + lane_base + 128 + b * 64 + half * 32, wd);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
       tc::mbar_arrive(&p_full[b]);
     }
     tc::mbar_wait(done, 0);
@@ -587,30 +655,26 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
+// dQ: one CTA per (128-query block, head), looping over 64-key blocks:
+// S = Q K_j^T, dP = dO V_j^T; dS = P (dP - delta) (bf16, over the dP columns
+// in TMEM); dQ += dS K_j with A from TMEM.
 template <int HD>
 __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ AttnBwdParams p) {
-  constexpr int NC = (HD + 63) / 64;
-  constexpr int Q_T = NC * CHUNK;        // [128 rows x hd]
-  constexpr int K_T = NC * CHUNK / 2;    // [64 rows x hd]
-  constexpr int KCH = CHUNK / 2;
-  constexpr int DS_T = CHUNK;            // [128 q x 64 keys]
+  constexpr int KST = dq_stages<HD>();
+  constexpr int Q_T = Lay<HD>::bytes(128), K_T = Lay<HD>::bytes(64);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int KST = 4;  // K/V ring depth
   uint8_t* sQ = sm;
   uint8_t* sdO = sQ + Q_T;
-  uint8_t* sK = sdO + Q_T;       // [KST]
-  uint8_t* sV = sK + KST * K_T;  // [KST]
-  uint8_t* sdS = sV + KST * K_T; // [2]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + 2 * DS_T);
+  uint8_t* sK = sdO + Q_T;        // [KST]
+  uint8_t* sV = sK + KST * K_T;   // [KST]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + KST * K_T);
   uint64_t* qo_full = bars;
   uint64_t* s_full = bars + 1;    // [2]
-  uint64_t* s_empty = bars + 3;   // [2]
   uint64_t* ds_full = bars + 5;   // [2]
-  uint64_t* ds_empty = bars + 7;  // [2]
   uint64_t* done = bars + 9;
-  uint64_t* kv_full = bars + 10;          // [KST]
-  uint64_t* kv_empty = kv_full + KST;     // [KST]
+  uint64_t* kv_full = bars + 10;       // [KST]
+  uint64_t* kv_empty = kv_full + KST;  // [KST]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + KST);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -627,9 +691,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ 
     tc::mbar_init(done, 1);
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&s_empty[i], 256);
       tc::mbar_init(&ds_full[i], 256);
-      tc::mbar_init(&ds_empty[i], 1);
     }
     for (int i = 0; i < KST; ++i) {
       tc::mbar_init(&kv_full[i], 1);
@@ -642,65 +704,55 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ 
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: S[2] at 0/64, dP[2] at 128/192, dQ at 256.
+  // TMEM: S[2] at 0/64, dP[2] at 128/192 (dS overwrites dP), dQ at 256.
 
   if (warp == 0) {
     if (lane == 0) {
-      tc::tma_prefetch(&p.tq);
-      tc::tma_prefetch(&p.tdo);
-      tc::tma_prefetch(&p.tkv);
+      tc::tma_prefetch(&p.tq.m0);
+      tc::tma_prefetch(&p.tdo.m0);
+      tc::tma_prefetch(&p.tkv.m0);
       tc::mbar_expect_tx(qo_full, 2 * Q_T);
-      for (int c = 0; c < NC; ++c) {
-        tc::tma_load_2d(sQ + c * CHUNK, &p.tq, qo_full, head * HD + 64 * c, static_cast<int>(q0));
-        tc::tma_load_2d(sdO + c * CHUNK, &p.tdo, qo_full, head * HD + 64 * c, static_cast<int>(q0));
-      }
+      load_tile<HD>(sQ, p.tq, qo_full, head * HD, static_cast<int>(q0), 128, 0);
+      load_tile<HD>(sdO, p.tdo, qo_full, head * HD, static_cast<int>(q0), 128, 0);
       for (int j = 0; j < nblk; ++j) {
         const int st = j % KST;
         tc::mbar_wait(&kv_empty[st], ((j / KST) & 1) ^ 1);
         tc::mbar_expect_tx(&kv_full[st], 2 * K_T);
-        for (int c = 0; c < NC; ++c) {
-          tc::tma_load_2d(sK + st * K_T + c * KCH, &p.tkv, &kv_full[st], head * HD + 64 * c, j * 64);
-          tc::tma_load_2d(sV + st * K_T + c * KCH, &p.tkv, &kv_full[st], p.h + head * HD + 64 * c, j * 64);
-        }
+        load_tile<HD>(sK + st * K_T, p.tkv, &kv_full[st], head * HD, j * 64, 64, 0);
+        load_tile<HD>(sV + st * K_T, p.tkv, &kv_full[st], p.h + head * HD, j * 64, 64, 0);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc_s = tc::idesc_bf16(128, 64, false, false);
-      constexpr uint32_t idesc_q = tc::idesc_bf16(128, HD, false, true);
       tc::mbar_wait(qo_full, 0);
       const uint32_t q_base = tc::smem_u32(sQ), do_base = tc::smem_u32(sdO);
-      int sj = 0, gj = 0;  // polled issue queues: S/dP of block sj, dQ += dS K of block gj
+      // Polled issue queues: S/dP of block sj (once dQ of block sj-2, which
+      // reads dS from the same TMEM buffer, is issued) and dQ += dS K of block gj.
+      int sj = 0, gj = 0;
       while (gj < nblk) {
-        if (sj < nblk && tc::mbar_test(&kv_full[sj % KST], (sj / KST) & 1) &&
-            tc::mbar_test(&s_empty[sj & 1], ((sj >> 1) & 1) ^ 1)) {
+        if (sj < nblk && sj < gj + 2 && tc::mbar_test(&kv_full[sj % KST], (sj / KST) & 1)) {
           const int j = sj++;
           const int b = j & 1, st = j % KST;
           tc::tc_fence_after();
           const uint32_t k_base = tc::smem_u32(sK + st * K_T), v_base = tc::smem_u32(sV + st * K_T);
 #pragma unroll
           for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint32_t off_q = (kk >> 2) * CHUNK + (kk & 3) * 32;
-            const uint32_t off_k = (kk >> 2) * KCH + (kk & 3) * 32;
-            tc::mma_bf16_ss(tmem + b * 64, tc::smem_desc(q_base + off_q, 16, 1024, tc::kSwizzle128B),
-                            tc::smem_desc(k_base + off_k, 16, 1024, tc::kSwizzle128B), idesc_s, kk > 0);
-            tc::mma_bf16_ss(tmem + 128 + b * 64, tc::smem_desc(do_base + off_q, 16, 1024, tc::kSwizzle128B),
-                            tc::smem_desc(v_base + off_k, 16, 1024, tc::kSwizzle128B), idesc_s, kk > 0);
+            tc::mma_bf16_ss(tmem + b * 64, kdesc<HD>(q_base, 128, kk), kdesc<HD>(k_base, 64, kk), idesc_s, kk > 0);
+            tc::mma_bf16_ss(tmem + 128 + b * 64, kdesc<HD>(do_base, 128, kk), kdesc<HD>(v_base, 64, kk), idesc_s,
+                            kk > 0);
           }
           tc::mma_commit(&s_full[b]);
           continue;
         }
         if (gj < sj && tc::mbar_test(&ds_full[gj & 1], (gj >> 1) & 1)) {
-          const int j = ++gj;  // j - 1 == the block being consumed (keeps the (j - 1) terms below)
-          const int b = (j - 1) & 1, st = (j - 1) % KST;
+          const int j = gj++;
+          const int b = j & 1, st = j % KST;
           tc::tc_fence_after();
-          const uint32_t ds = tc::smem_u32(sdS + b * DS_T), k_base = tc::smem_u32(sK + st * K_T);
+          const uint32_t k_base = tc::smem_u32(sK + st * K_T);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)  // K = 64 keys
-            tc::mma_bf16_ss(tmem + 256, tc::smem_desc(ds + kk * 32, 16, 1024, tc::kSwizzle128B),
-                            tc::smem_desc(k_base + kk * 2048, KCH, 1024, tc::kSwizzle128B), idesc_q,
-                            (j - 1) > 0 || kk > 0);
-          tc::mma_commit(&ds_empty[b]);
+            mma_nhd_ts<HD>(tmem + 256, tmem + 128 + b * 64 + half_packed_col(kk), k_base, 64, kk, j > 0 || kk > 0);
           tc::mma_commit(&kv_empty[st]);
         }
       }
@@ -729,9 +781,6 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ 
       tc::tmem_ld32(tmem + lane_base + b * 64 + half * 32, sv);
       tc::tmem_ld32(tmem + lane_base + 128 + b * 64 + half * 32, dpv);
       tc::tmem_ld_wait();
-      tc::tc_fence_before();
-      tc::mbar_arrive(&s_empty[b]);
-      tc::mbar_wait(&ds_empty[b], ph ^ 1);
       const bool full_blk = __all_sync(0xffffffffu, lim >= 31);
       uint32_t w[16];
 #pragma unroll
@@ -746,31 +795,30 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ 
         }
         w[e / 2] = pack_bf16(d2[0], d2[1]);
       }
-      st_tile_row32(sdS + b * DS_T, r, half, w);
-      fence_async_smem();
+      tc::tmem_st16(tmem + lane_base + 128 + b * 64 + half * 32, w);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
       tc::mbar_arrive(&ds_full[b]);
     }
     tc::mbar_wait(done, 0);
     tc::tc_fence_after();
-    {
-      __nv_bfloat16* dq_row = p.dq + (valid ? row : 0) * p.h + head * HD;
-      constexpr int NCH = HD / 16, SPLIT = (NCH + 1) / 2;
-      for (int c = half ? SPLIT : 0; c < (half ? NCH : SPLIT); ++c) {
-        uint32_t v[16];
-        tmem_ld16(tmem + lane_base + 256 + c * 16, v);  // warp-collective: all lanes
-        tc::tmem_ld_wait();
-        if (!valid) continue;
-        uint4 u0 = make_uint4(pack_bf16(__uint_as_float(v[0]) * p.scale, __uint_as_float(v[1]) * p.scale),
-                              pack_bf16(__uint_as_float(v[2]) * p.scale, __uint_as_float(v[3]) * p.scale),
-                              pack_bf16(__uint_as_float(v[4]) * p.scale, __uint_as_float(v[5]) * p.scale),
-                              pack_bf16(__uint_as_float(v[6]) * p.scale, __uint_as_float(v[7]) * p.scale));
-        uint4 u1 = make_uint4(pack_bf16(__uint_as_float(v[8]) * p.scale, __uint_as_float(v[9]) * p.scale),
-                              pack_bf16(__uint_as_float(v[10]) * p.scale, __uint_as_float(v[11]) * p.scale),
-                              pack_bf16(__uint_as_float(v[12]) * p.scale, __uint_as_float(v[13]) * p.scale),
-                              pack_bf16(__uint_as_float(v[14]) * p.scale, __uint_as_float(v[15]) * p.scale));
-        *reinterpret_cast<uint4*>(dq_row + c * 16) = u0;
-        *reinterpret_cast<uint4*>(dq_row + c * 16 + 8) = u1;
-      }
+    __nv_bfloat16* dq_row = p.dq + (valid ? row : 0) * p.h + head * HD;
+    constexpr int NCH = HD / 16, SPLIT = (NCH + 1) / 2;
+    for (int c = half ? SPLIT : 0; c < (half ? NCH : SPLIT); ++c) {
+      uint32_t v[16];
+      tmem_ld16(tmem + lane_base + 256 + c * 16, v);  // warp-collective: all lanes
+      tc::tmem_ld_wait();
+      if (!valid) continue;
+      uint4 u0 = make_uint4(pack_bf16(__uint_as_float(v[0]) * p.scale, __uint_as_float(v[1]) * p.scale),
+                            pack_bf16(__uint_as_float(v[2]) * p.scale, __uint_as_float(v[3]) * p.scale),
+                            pack_bf16(__uint_as_float(v[4]) * p.scale, __uint_as_float(v[5]) * p.scale),
+                            pack_bf16(__uint_as_float(v[6]) * p.scale, __uint_as_float(v[7]) * p.scale));
+      uint4 u1 = make_uint4(pack_bf16(__uint_as_float(v[8]) * p.scale, __uint_as_float(v[9]) * p.scale),
+                            pack_bf16(__uint_as_float(v[10]) * p.scale, __uint_as_float(v[11]) * p.scale),
+                            pack_bf16(__uint_as_float(v[12]) * p.scale, __uint_as_float(v[13]) * p.scale),
+                            pack_bf16(__uint_as_float(v[14]) * p.scale, __uint_as_float(v[15]) * p.scale));
+      *reinterpret_cast<uint4*>(dq_row + c * 16) = u0;
+      *reinterpret_cast<uint4*>(dq_row + c * 16 + 8) = u1;
     }
   }
   tc::tc_fence_before();
@@ -779,62 +827,6 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ 
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-void make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems, uint32_t rows = 128) {
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld_elems * 2};
-  cuuint32_t box[2] = {64, rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = tma_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (attention) failed: " + std::to_string((int)r));
-}
-
-template <int HD>
-size_t fwd_smem_bytes() {
-  constexpr int NC = (HD + 63) / 64;
-  return NC * CHUNK * 5 + 4 * CHUNK + 1024 + 256;
-}
-
-template <int HD>
-void launch_fwd(const AttnParams& p, cudaStream_t s) {
-  const size_t smem = fwd_smem_bytes<HD>();
-  SPK_CUDA(cudaFuncSetAttribute(attn_fwd_tc_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid(static_cast<unsigned>((p.n + BQ - 1) / BQ), static_cast<unsigned>(p.H));
-  attn_fwd_tc_k<HD><<<grid, 256, smem, s>>>(p);
-  SPK_LAUNCH_CHECK();
-}
-
-}  // namespace
-
-bool attn_tc_supported(DType t, int hd) { return t == DType::kBF16 && (hd == 64 || hd == 80 || hd == 128); }
-
-void attn_fwd_tc(const void* q, const void* kv, void* o, float* lse, int64_t n, int64_t q_off, int64_t kv_len, int H,
-                 int hd, cudaStream_t s) {
-  AttnParams p;
-  const int h = H * hd;
-  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kv) | reinterpret_cast<uintptr_t>(o)) & 15)
-    throw std::invalid_argument("attention: operands must be 16-byte aligned");
-  make_map(&p.tq, q, h, n, h);
-  make_map(&p.tkv, kv, 2 * h, kv_len, 2 * h);
-  p.o = static_cast<__nv_bfloat16*>(o);
-  p.lse = lse;
-  p.n = n;
-  p.q_off = q_off;
-  p.kv_len = kv_len;
-  p.H = H;
-  p.hd = hd;
-  p.h = h;
-  p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(hd));
-  switch (hd) {
-    case 64: launch_fwd<64>(p, s); break;
-    case 80: launch_fwd<80>(p, s); break;
-    case 128: launch_fwd<128>(p, s); break;
-    default: throw std::invalid_argument("attention tc: head_dim must be 64, 80 or 128");
-  }
-}
-
-namespace {
 // ld[head][i] = (lse * log2e, sum_d dO*O) for i < n, zeros up to n_pad: the
 // per-query vectors the backward kernels stream (one warp per (i, head)).
 __global__ void attn_prep_k(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
@@ -854,7 +846,66 @@ __global__ void attn_prep_k(const __nv_bfloat16* __restrict__ o, const __nv_bflo
   }
   if (lane == 0) *reinterpret_cast<float2*>(ld + (head * n_pad + i) * 2) = make_float2(l, d);
 }
+
+// ---------------------------------------------------------------------------- host
+
+void make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems, uint32_t box_inner,
+              uint32_t rows, CUtensorMapSwizzle sw) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_inner, rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = tma_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (attention) failed: " + std::to_string((int)r));
+}
+
+// Chunk maps of a [outer, inner] bf16 tensor for [rows x hd] tiles.
+void make_maps(Maps* t, const void* ptr, uint64_t inner, uint64_t outer, int hd, uint32_t rows) {
+  make_map(&t->m0, ptr, inner, outer, inner, 64, rows, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (hd == 80 && Lay<80>::NARROW)
+    make_map(&t->m1, ptr, inner, outer, inner, 16, rows, CU_TENSOR_MAP_SWIZZLE_32B);
+  else
+    t->m1 = t->m0;  // second chunk = another 64-wide SW128 box (hd 80: padded); hd 64: unused
+}
+
 }  // namespace
+
+bool attn_tc_supported(DType t, int hd) { return t == DType::kBF16 && (hd == 64 || hd == 80 || hd == 128); }
+
+void attn_fwd_tc(const void* q, const void* kv, void* o, float* lse, int64_t n, int64_t q_off, int64_t kv_len, int H,
+                 int hd, cudaStream_t s) {
+  AttnParams p;
+  const int h = H * hd;
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kv) | reinterpret_cast<uintptr_t>(o)) & 15)
+    throw std::invalid_argument("attention: operands must be 16-byte aligned");
+  make_maps(&p.tq, q, h, n, hd, 128);
+  make_maps(&p.tkv, kv, 2 * h, kv_len, hd, 128);
+  p.o = static_cast<__nv_bfloat16*>(o);
+  p.lse = lse;
+  p.n = n;
+  p.q_off = q_off;
+  p.kv_len = kv_len;
+  p.H = H;
+  p.h = h;
+  p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(hd));
+  auto run = [&](auto hd_tag) {
+    constexpr int HD = decltype(hd_tag)::value;
+    constexpr size_t smem = fwd_smem<HD>();
+    static_assert(smem <= 232448, "attention fwd smem");
+    SPK_CUDA(cudaFuncSetAttribute(attn_fwd_tc_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid(static_cast<unsigned>((n + BQ - 1) / BQ), static_cast<unsigned>(H));
+    attn_fwd_tc_k<HD><<<grid, 256, smem, s>>>(p);
+    SPK_LAUNCH_CHECK();
+  };
+  switch (hd) {
+    case 64: run(std::integral_constant<int, 64>{}); break;
+    case 80: run(std::integral_constant<int, 80>{}); break;
+    case 128: run(std::integral_constant<int, 128>{}); break;
+    default: throw std::invalid_argument("attention tc: head_dim must be 64, 80 or 128");
+  }
+}
 
 size_t attn_bwd_ws_delta_floats(int64_t n, int H) { return static_cast<size_t>(H) * ((n + 63) / 64 * 64) * 2; }
 
@@ -865,6 +916,7 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kv) | reinterpret_cast<uintptr_t>(dout) |
        reinterpret_cast<uintptr_t>(dq) | reinterpret_cast<uintptr_t>(dkv)) & 15)
     throw std::invalid_argument("attention: operands must be 16-byte aligned");
+  (void)ws_dq;
   const int64_t n_pad = (n + 63) / 64 * 64;
   {
     const int64_t warps = n_pad * H;
@@ -872,11 +924,11 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
         static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, ws_delta, n, n_pad, H, hd);
     SPK_LAUNCH_CHECK();
   }
-  // dKV kernel: Q/dO boxes of 64 rows, KV boxes of 128 rows; dQ kernel: the reverse.
+  // dKV kernel: Q/dO tiles of 64 rows, K/V tiles of 128 rows; dQ kernel: the reverse.
   AttnBwdParams a;
-  make_map(&a.tq, q, h, n, h, 64);
-  make_map(&a.tdo, dout, h, n, h, 64);
-  make_map(&a.tkv, kv, 2 * h, kv_len, 2 * h, 128);
+  make_maps(&a.tq, q, h, n, hd, 64);
+  make_maps(&a.tdo, dout, h, n, hd, 64);
+  make_maps(&a.tkv, kv, 2 * h, kv_len, hd, 128);
   a.ld = ws_delta;
   a.n_pad = n_pad;
   a.dkv = dkv;
@@ -894,17 +946,13 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
   }();
   a.dbg = dbg;
   AttnBwdParams b = a;
-  make_map(&b.tq, q, h, n, h, 128);
-  make_map(&b.tdo, dout, h, n, h, 128);
-  make_map(&b.tkv, kv, 2 * h, kv_len, 2 * h, 64);
-  (void)ws_dq;
+  make_maps(&b.tq, q, h, n, hd, 128);
+  make_maps(&b.tdo, dout, h, n, hd, 128);
+  make_maps(&b.tkv, kv, 2 * h, kv_len, hd, 64);
   auto run = [&](auto hd_tag) {
     constexpr int HD = decltype(hd_tag)::value;
-    constexpr int NC = (HD + 63) / 64;
-    constexpr int QST = NC == 1 ? 4 : 3, KST = 4;
-    const size_t smem_dkv = 2 * NC * CHUNK + 2 * QST * (NC * CHUNK / 2) + 4 * CHUNK + QST * 512 + (10 + 2 * QST) * 8 + 8 +
-                            1024;
-    const size_t smem_dq = 2 * NC * CHUNK + 2 * KST * (NC * CHUNK / 2) + 2 * CHUNK + (6 + 2 * KST) * 8 + 8 + 1024;
+    constexpr size_t smem_dkv = dkv_smem<HD>(), smem_dq = dq_smem<HD>();
+    static_assert(smem_dkv <= 232448 && smem_dq <= 232448, "attention bwd smem");
     SPK_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dkv));
     SPK_CUDA(cudaFuncSetAttribute(attn_bwd_dq_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dq));
     {
@@ -923,7 +971,6 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
       lc.numAttrs = 1;
       SPK_CUDA(cudaLaunchKernelEx(&lc, attn_bwd_dkv_k<HD>, a));
     }
-    SPK_LAUNCH_CHECK();
     dim3 g2(static_cast<unsigned>((n + 127) / 128), static_cast<unsigned>(H));
     attn_bwd_dq_k<HD><<<g2, 384, smem_dq, s>>>(b);
     SPK_LAUNCH_CHECK();

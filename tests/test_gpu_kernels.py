@@ -84,7 +84,10 @@ def _attn_ref(q, kv, n, q_off, H, hd):
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("impl", [1, 0])
-@pytest.mark.parametrize("n,q_off,H,hd", [(77, 0, 2, 64), (130, 200, 4, 64), (96, 160, 3, 80), (200, 57, 2, 128)])
+@pytest.mark.parametrize("n,q_off,H,hd", [(77, 0, 2, 64), (130, 200, 4, 64), (96, 160, 3, 80), (200, 57, 2, 128),
+                                          # long prefixes: every SMEM ring wraps several times
+                                          (515, 1300, 2, 64), (700, 1111, 2, 80), (1000, 0, 2, 80),
+                                          (333, 1500, 2, 128)])
 def test_attention_fwd_bwd(gpu, dtype, impl, n, q_off, H, hd):
     g = torch.Generator(device="cuda").manual_seed(n + q_off)
     h = H * hd

@@ -83,10 +83,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--attn", action="store_true")
+    ap.add_argument("--attn-only", action="store_true")
     args = ap.parse_args()
+    args.attn |= args.attn_only
     shapes = [("2.7b", 10170, 2560, 10240), ("7b", 11428, 4096, 11008), ("13b", 14094, 5120, 20480)]
     if args.quick:
         shapes = shapes[:1]
+    if args.attn_only:
+        shapes = []
     for name, n, h, F in shapes:
         for role, (M, N, K, ak, bk, cf, acc) in {
             "qkv_fwd": (n, 3 * h, h, 1, 1, 0, 0),
