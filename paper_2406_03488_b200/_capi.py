@@ -168,7 +168,11 @@ def lib():
         if not LIB_PATH.exists():
             raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2406_03488_b200.build` "
                                "(no CPU/Python fallback exists)")
-        _lib = C.CDLL(str(LIB_PATH))
+        path = LIB_PATH
+        variant = os.environ.get("SP_LIB_VARIANT")  # kernel-tuning builds (tools/build_variant.py)
+        if variant:
+            path = LIB_PATH.parent / "variants" / f"libseqpipe_b200_{variant}.so"
+        _lib = C.CDLL(str(path))
         for name, (res, args) in _SIGS.items():
             fn = getattr(_lib, name, None)
             if fn is None:

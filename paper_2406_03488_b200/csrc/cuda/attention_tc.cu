@@ -24,7 +24,9 @@
 // both deterministic, no atomics.
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "cuda/common.cuh"
 #include "cuda/ops.h"
@@ -39,7 +41,7 @@ namespace {
 constexpr int BQ = 128, BKV = 128;
 
 #ifndef SPK_ATTN_NARROW80
-#define SPK_ATTN_NARROW80 0  // measured slower on B200 (extra N=16 MMAs, 32-byte TMA rows)
+#define SPK_ATTN_NARROW80 0  // hd 80 as 64 + 16 columns (SW128 + SW32): measured slower (N=16 MMAs, 32-byte TMA rows)
 #endif
 
 template <int HD>
@@ -66,11 +68,11 @@ template <int HD>
 __device__ __forceinline__ void mma_nhd(uint32_t d, uint64_t adesc, uint32_t bbase, int rows, int kk, bool acc) {
   if constexpr (Lay<HD>::NARROW) {
     constexpr uint32_t i64 = tc::idesc_bf16(128, 64, false, true), i16 = tc::idesc_bf16(128, 16, false, true);
-    tc::mma_bf16_ss(d, adesc, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), i64, acc);
-    tc::mma_bf16_ss(d + 64, adesc, tc::smem_desc(bbase + rows * 128 + kk * 512, 256, 256, tc::kSwizzle32B), i16, acc);
+    tc::mma_bf16_ss_w(d, adesc, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), i64, acc);
+    tc::mma_bf16_ss_w(d + 64, adesc, tc::smem_desc(bbase + rows * 128 + kk * 512, 256, 256, tc::kSwizzle32B), i16, acc);
   } else {  // padded second chunk: one N = hd MMA
     constexpr uint32_t id = tc::idesc_bf16(128, HD, false, true);
-    tc::mma_bf16_ss(d, adesc, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), id, acc);
+    tc::mma_bf16_ss_w(d, adesc, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), id, acc);
   }
 }
 
@@ -79,18 +81,21 @@ template <int HD>
 __device__ __forceinline__ void mma_nhd_ts(uint32_t d, uint32_t a_tmem, uint32_t bbase, int rows, int kk, bool acc) {
   if constexpr (Lay<HD>::NARROW) {
     constexpr uint32_t i64 = tc::idesc_bf16(128, 64, false, true), i16 = tc::idesc_bf16(128, 16, false, true);
-    tc::mma_bf16_ts(d, a_tmem, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), i64, acc);
-    tc::mma_bf16_ts(d + 64, a_tmem, tc::smem_desc(bbase + rows * 128 + kk * 512, 256, 256, tc::kSwizzle32B), i16, acc);
+    tc::mma_bf16_ts_w(d, a_tmem, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), i64, acc);
+    tc::mma_bf16_ts_w(d + 64, a_tmem, tc::smem_desc(bbase + rows * 128 + kk * 512, 256, 256, tc::kSwizzle32B), i16, acc);
   } else {
     constexpr uint32_t id = tc::idesc_bf16(128, HD, false, true);
-    tc::mma_bf16_ts(d, a_tmem, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), id, acc);
+    tc::mma_bf16_ts_w(d, a_tmem, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), id, acc);
   }
 }
 
-// TMEM column of K-step kk (16 columns of a 64-wide bf16 operand) when each
-// half (32 columns) of the operand was packed at the start of its own 32
-// fp32 columns (the softmax half that produced it overwrites only its slice).
-__device__ __forceinline__ uint32_t half_packed_col(int kk) { return 32 * (kk >> 1) + 8 * (kk & 1); }
+
+// One arrive per warp (count barriers in warps): a 512-thread arrive costs
+// hundreds of cycles of shared-memory atomics per phase.
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) tc::mbar_arrive(bar);
+}
 
 __device__ __forceinline__ float4 lds_f4(const void* p) {
   float4 v;
@@ -149,6 +154,83 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2: two lanes per issue
+// slot) and the 3-input max (FMNMX3). The softmax loops are issue-bound, so
+// these halve their FMA-pipe instruction count.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 a, b, c, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+      "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float2 u2f2(uint32_t a, uint32_t b) { return make_float2(__uint_as_float(a), __uint_as_float(b)); }
+__device__ __forceinline__ uint32_t pack2(float2 v) { return pack_bf16(v.x, v.y); }
+__device__ __forceinline__ float2 ex2x2(float2 v) { return make_float2(ex2(v.x), ex2(v.y)); }
+
+// exp2 of a pair on the FMA pipe (no MUFU): x = j + f with j = rint(x) (magic-number
+// add), 2^f on [-0.5, 0.5] by a degree-3 polynomial (max relative error 7.7e-5,
+// far below the bf16 rounding of P), then j added into the exponent field.
+// Inputs are clamped at -126 (2^-126 ~ 1e-38 stands in for 0). The softmax loops
+// send a fixed fraction of their exponentials here so the MUFU pipe (16/clk/SM)
+// stops being the bound at head_dim 80.
+__device__ __forceinline__ float2 ex2x2_poly(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));        // 1.5 * 2^23 + rint(x)
+  const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));      // rint(x)
+  const float2 f = ffma2(j, make_float2(-1.f, -1.f), x);                 // x - rint(x) in [-0.5, 0.5]
+  float2 q = ffma2(make_float2(0.05508868f, 0.05508868f), f, make_float2(0.24260405f, 0.24260405f));
+  q = ffma2(q, f, make_float2(0.69327624f, 0.69327624f));
+  q = ffma2(q, f, make_float2(0.99992894f, 0.99992894f));
+  // low bits of t are rint(x) (two's complement), so t << 23 is rint(x) << 23
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
+}
+// `poly` is a constant after the softmax loops are unrolled.
+__device__ __forceinline__ float2 ex2x2_sel(bool poly, float2 v) { return poly ? ex2x2_poly(v) : ex2x2(v); }
+// Which groups of a fully unrolled softmax loop use the FMA-pipe exponential: 3 of 8.
+#ifndef SPK_POLY_FWD
+#define SPK_POLY_FWD 3
+#endif
+#ifndef SPK_POLY_BWD
+#define SPK_POLY_BWD 0
+#endif
+#ifndef SPK_POLY_DQ
+#define SPK_POLY_DQ SPK_POLY_BWD
+#endif
+// Which 4-element groups of a fully unrolled softmax loop use the FMA-pipe
+// exponential: SPK_POLY_* of every 8, spread out.
+__host__ __device__ constexpr bool poly_pick(int g, int k) { return (g % 8) * k % 8 + k > 7 || (k >= 8); }
+__host__ __device__ constexpr bool poly_group(int g) { return SPK_POLY_FWD > 0 && poly_pick(g, SPK_POLY_FWD); }
+__host__ __device__ constexpr bool bwd_poly_group(int g) { return SPK_POLY_BWD > 0 && poly_pick(g, SPK_POLY_BWD); }
+__host__ __device__ constexpr bool dq_poly_group(int g) { return SPK_POLY_DQ > 0 && poly_pick(g, SPK_POLY_DQ); }
+
 template <int HD>
 constexpr size_t fwd_smem_n(int st) {
   return Lay<HD>::bytes(128) * (1 + 2 * st) + (10 + 4 * st) * 8 + 8 + 1024;
@@ -156,7 +238,7 @@ constexpr size_t fwd_smem_n(int st) {
 // Ring depths: as many stages as the opt-in SMEM (227 KB) holds, capped at 4 / 6 / 8.
 template <int HD>
 constexpr int fwd_stages() {
-  int st = 4;
+  int st = 6;
   while (fwd_smem_n<HD>(st) > 232448) --st;
   return st;
 }
@@ -200,7 +282,7 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
     tc::mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&p_full[i], 128);
+      tc::mbar_init(&p_full[i], 4);  // softmax warps
       tc::mbar_init(&p_empty[i], 1);
     }
     for (int i = 0; i < KVS; ++i) {
@@ -215,7 +297,7 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform (keeps MMA operands in uniform registers)
   // TMEM: S0 [0,128) S1 [128,256) O [256, 256+hd). P_j (bf16) overwrites the
   // first 64 columns of its S buffer and feeds the PV MMA straight from TMEM.
 
@@ -243,39 +325,38 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp, converged: tc::*_w helpers elect the issuing lane
       constexpr uint32_t idesc_s = tc::idesc_bf16(128, BKV, false, false);
-      tc::mbar_wait(q_full, 0);
+      tc::mbar_wait_w(q_full, 0);
       const uint32_t q_base = tc::smem_u32(sQ);
-      // Poll two queues: S_j (needs K_j, and PV_{j-2} issued: S_j overwrites
-      // the buffer P_{j-2} is read from; MMAs execute in issue order) and PV_j
-      // (needs P_j and V_j).
-      int sj = 0, pj = 0;
-      while (pj < nblk) {
-        if (sj < nblk && sj < pj + 2 && tc::mbar_test(&k_full[sj % KVS], (sj / KVS) & 1)) {
-          const int b = sj & 1, st = sj % KVS;
-          tc::tc_fence_after();
-          const uint32_t k_base = tc::smem_u32(sK + st * TB);
+      // Static issue order with blocking waits (an mbarrier try_wait wakes ~60
+      // cycles after the arrive; polling with test_wait costs ~150 per probe):
+      // S_0, S_1, then per block j: PV_j once P_j is in TMEM, then S_{j+2} into
+      // the buffer PV_j just read (MMAs execute in issue order).
+      auto issue_s = [&](int j) {
+        const int b = j & 1, st = j % KVS;
+        tc::mbar_wait_w(&k_full[st], (j / KVS) & 1);
+        tc::tc_fence_after();
+        const uint32_t k_base = tc::smem_u32(sK + st * TB);
 #pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk)
-            tc::mma_bf16_ss(tmem + b * 128, kdesc<HD>(q_base, 128, kk), kdesc<HD>(k_base, 128, kk), idesc_s, kk > 0);
-          tc::mma_commit(&s_full[b]);
-          tc::mma_commit(&k_empty[st]);
-          ++sj;
-          continue;
-        }
-        if (pj < sj && tc::mbar_test(&p_full[pj & 1], (pj >> 1) & 1) &&
-            tc::mbar_test(&v_full[pj % KVS], (pj / KVS) & 1)) {
-          const int b = pj & 1, st = pj % KVS;
-          tc::tc_fence_after();
-          const uint32_t v_base = tc::smem_u32(sV + st * TB);
+        for (int kk = 0; kk < HD / 16; ++kk)
+          tc::mma_bf16_ss_w(tmem + b * 128, kdesc<HD>(q_base, 128, kk), kdesc<HD>(k_base, 128, kk), idesc_s, kk > 0);
+        tc::mma_commit_w(&s_full[b]);
+        tc::mma_commit_w(&k_empty[st]);
+      };
+      for (int j = 0; j < 2 && j < nblk; ++j) issue_s(j);
+      for (int j = 0; j < nblk; ++j) {
+        const int b = j & 1, st = j % KVS;
+        tc::mbar_wait_w(&p_full[b], (j >> 1) & 1);
+        tc::mbar_wait_w(&v_full[st], (j / KVS) & 1);
+        tc::tc_fence_after();
+        const uint32_t v_base = tc::smem_u32(sV + st * TB);
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk)  // O accumulates in TMEM; A = P_j from TMEM
-            mma_nhd_ts<HD>(tmem + 256, tmem + b * 128 + kk * 8, v_base, 128, kk, pj > 0 || kk > 0);
-          tc::mma_commit(&p_empty[b]);  // also marks PV_pj (and every earlier MMA) complete
-          tc::mma_commit(&v_empty[st]);
-          ++pj;
-        }
+        for (int kk = 0; kk < BKV / 16; ++kk)  // O accumulates in TMEM; A = P_j from TMEM
+          mma_nhd_ts<HD>(tmem + 256, tmem + b * 128 + kk * 8, v_base, 128, kk, j > 0 || kk > 0);
+        tc::mma_commit_w(&p_empty[b]);  // also marks PV_j (and every earlier MMA) complete
+        tc::mma_commit_w(&v_empty[st]);
+        if (j + 2 < nblk) issue_s(j + 2);
       }
     }
   } else if (warp >= 4) {
@@ -307,16 +388,22 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
       tc::tmem_ld_wait();
       // Raw scores stay unscaled (scale > 0 commutes with max); masking only on
       // blocks that touch the causal diagonal or the prefix end.
-      float mx = -INFINITY;
-      if (__all_sync(0xffffffffu, lim >= BKV - 1)) {
+      if (!__all_sync(0xffffffffu, lim >= BKV - 1)) {
 #pragma unroll
-        for (int c = 0; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(sv[c]));
-      } else {
-#pragma unroll
-        for (int c = 0; c < 128; ++c) {
+        for (int c = 0; c < 128; ++c)
           if (c > lim) sv[c] = __float_as_uint(-INFINITY);
-          mx = fmaxf(mx, __uint_as_float(sv[c]));
+      }
+      float mx;
+      {  // four independent FMNMX3 chains
+        float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 128; c += 8) {
+          m0 = fmax3(m0, __uint_as_float(sv[c]), __uint_as_float(sv[c + 1]));
+          m1 = fmax3(m1, __uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3]));
+          m2 = fmax3(m2, __uint_as_float(sv[c + 4]), __uint_as_float(sv[c + 5]));
+          m3 = fmax3(m3, __uint_as_float(sv[c + 6]), __uint_as_float(sv[c + 7]));
         }
+        mx = fmax3(m0, m1, fmaxf(m2, m3));
       }
       mx *= p.scale_log2;
       const bool need = (m == -INFINITY) ? (mx > -INFINITY || j == 0) : (mx > m + kRescale);
@@ -344,24 +431,27 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
         m = m_new;
       }
       const float neg_m = m == -INFINITY ? 0.f : -m;
-      float rs0 = 0.f, rs1 = 0.f;
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(neg_m, neg_m);
+      float2 rs_a = make_float2(0.f, 0.f), rs_b = make_float2(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t w[16];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(sv[c * 32 + e]), p.scale_log2, neg_m));
-          const float p1 = ex2(fmaf(__uint_as_float(sv[c * 32 + e + 1]), p.scale_log2, neg_m));
-          rs0 += p0;
-          rs1 += p1;
-          w[e / 2] = pack_bf16(p0, p1);
+        for (int e = 0; e < 32; e += 4) {
+          const bool poly = poly_group(c * 8 + e / 4);
+          const float2 x0 = ex2x2_sel(poly, ffma2(u2f2(sv[c * 32 + e], sv[c * 32 + e + 1]), sc2, nm2));
+          const float2 x1 = ex2x2_sel(poly, ffma2(u2f2(sv[c * 32 + e + 2], sv[c * 32 + e + 3]), sc2, nm2));
+          rs_a = fadd2(rs_a, x0);
+          rs_b = fadd2(rs_b, x1);
+          w[e / 2] = pack2(x0);
+          w[e / 2 + 1] = pack2(x1);
         }
         tc::tmem_st16(sbase + c * 16, w);  // P keys [32c, 32c+32) -> columns [16c, 16c+16)
       }
-      l += rs0 + rs1;
+      l += (rs_a.x + rs_a.y) + (rs_b.x + rs_b.y);
       tc::tmem_st_wait();
       tc::tc_fence_before();
-      tc::mbar_arrive(&p_full[b]);
+      warp_arrive(&p_full[b]);
     }
     if (nblk > 0) tc::mbar_wait(&p_empty[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);  // last PV landed
     tc::tc_fence_after();
@@ -395,26 +485,57 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
 // ============================================================================ backward
 
 struct __align__(64) AttnBwdParams {
+  CUtensorMap tdkv;  // dkv fp32 [kv_len, 2h], [128 x HD] boxes (TMA reduce-add of dK / dV)
   Maps tq;           // q  [n, h]
   Maps tdo;          // dO [n, h]
   Maps tkv;          // kv [kv_len, 2h]
-  const float* ld;   // [H, n_pad] x (LSE * log2e, delta), zero padded (attn_prep_k)
-  int64_t n_pad;     // n rounded up to 64
+  const __nv_bfloat16 *q, *dout, *kv;  // raw rows (copied into TMEM as constant MMA operands)
+  const float* ld;   // [H][n_pad / 64][-LSE*log2e x 64, -delta x 64], zero padded (attn_prep_k)
+  int64_t n_pad;     // n rounded up to 128
   float* dkv;        // [kv_len, 2h] fp32 accumulator
   __nv_bfloat16* dq; // [n, h]
   int64_t n, q_off, kv_len;
   int H, h;
   float scale, scale_log2;
-  int dbg;  // profiling only (SP_ATTN_DBG): 1 = skip dK/dV MMAs, 2 = skip dK/dV softmax math
+  int dbg;  // profiling only (SP_ATTN_DBG): 1 = skip dK/dV MMAs, 2 = skip the dK/dV softmax (TMEM ld/st + math)
+  unsigned long long* trace;  // profiling only (SP_ATTN_TRACE): cycle stamps of one CTA, [event][iteration]
+};
+
+// ---------------------------------------------------------------- backward layout
+// dK/dV kernel (CTA = 128 keys, loops over 64-query blocks) and dQ kernel
+// (CTA = 128 queries, loops over 64-key blocks). In both, the operand that is
+// constant for the CTA (K and V, resp. Q and dO) is copied once into TMEM and
+// used as the A operand of the S / dP MMAs (128x64x16 "TS" MMAs run at the
+// tensor floor, 32 cycles; the SS form reads A and B from shared memory and is
+// bound at 48 cycles by the 128 B/cycle SMEM port). TMEM (512 columns):
+//   S[NS] x 64 | dP[ND] x 64 | accumulators | constant operands (bf16 pairs).
+// P / dS are packed (bf16) back into the score buffer they came from; the dP
+// buffer is released as soon as the softmax warps have loaded it.
+template <int HD>
+struct DkvCfg {
+  static constexpr bool KVT = HD <= 80;  // K, V in TMEM (hd 128: no room; SS form)
+  static constexpr int NS = KVT ? 3 : 2, ND = KVT ? 1 : 2;
+  static constexpr uint32_t T_DP = NS * 64, T_DV = T_DP + ND * 64;
+  static constexpr uint32_t T_DK = T_DV + (HD == 80 ? 96 : HD);
+  static constexpr uint32_t T_K = T_DK + HD, T_V = T_K + HD / 2;
+  static_assert((KVT ? T_V + HD / 2 : T_DK + HD) <= 512, "dK/dV TMEM budget");
+};
+template <int HD>
+struct DqCfg {
+  static constexpr int NS = HD == 128 ? 2 : 3, ND = HD == 128 ? 2 : 1;
+  static constexpr uint32_t T_DP = NS * 64, T_DQ = T_DP + ND * 64;
+  static constexpr uint32_t T_Q = T_DQ + (HD == 80 ? 96 : HD), T_DO = T_Q + HD / 2;
+  static_assert(T_DO + HD / 2 <= 512, "dQ TMEM budget");
 };
 
 template <int HD>
 constexpr size_t dkv_smem_n(int st) {
-  return 2 * Lay<HD>::bytes(128) + 2 * st * Lay<HD>::bytes(64) + st * 512 + (10 + 2 * st) * 8 + 8 + 1024;
+  return (DkvCfg<HD>::KVT ? 0 : 2 * Lay<HD>::bytes(128)) + 2 * st * Lay<HD>::bytes(64) + st * 512 + (16 + 2 * st) * 8 +
+         8 + 1024;
 }
 template <int HD>
 constexpr int dkv_stages() {
-  int st = 6;
+  int st = 8;
   while (dkv_smem_n<HD>(st) > 232448) --st;
   return st;
 }
@@ -424,7 +545,7 @@ constexpr size_t dkv_smem() {
 }
 template <int HD>
 constexpr size_t dq_smem_n(int st) {
-  return 2 * Lay<HD>::bytes(128) + 2 * st * Lay<HD>::bytes(64) + (10 + 2 * st) * 8 + 8 + 1024;
+  return 2 * st * Lay<HD>::bytes(64) + (16 + 2 * st) * 8 + 8 + 1024;
 }
 template <int HD>
 constexpr int dq_stages() {
@@ -437,31 +558,80 @@ constexpr size_t dq_smem() {
   return dq_smem_n<HD>(dq_stages<HD>());
 }
 
+// Debug timeline (SP_ATTN_TRACE=1): clock64 stamps of the last CTA of head 0,
+// 16 events x 64 iterations; printed by the host after the launch.
+__device__ __forceinline__ void trace_mark(const AttnBwdParams& p, int ev, int it) {
+  // every lane stores the same stamp: no lane-divergent branch in the MMA warp
+  if (p.trace && it < 64 && blockIdx.x == gridDim.x - 1 && blockIdx.y == 0) p.trace[ev * 64 + it] = clock64();
+}
+
+// Copy this lane's [HD] bf16 row (`src`, or zeros when !valid) into TMEM as an
+// MMA A operand: column c of the lane holds elements (2c, 2c+1).
+template <int HD>
+__device__ __forceinline__ void row_to_tmem(uint32_t taddr, const __nv_bfloat16* src, bool valid) {
+  uint32_t v[HD / 2];
+#pragma unroll
+  for (int c = 0; c < HD / 8; ++c) {
+    const uint4 u = valid ? __ldg(reinterpret_cast<const uint4*>(src) + c) : make_uint4(0, 0, 0, 0);
+    v[4 * c] = u.x;
+    v[4 * c + 1] = u.y;
+    v[4 * c + 2] = u.z;
+    v[4 * c + 3] = u.w;
+  }
+#pragma unroll
+  for (int c = 0; c < HD / 16; ++c) tc::tmem_st8(taddr + 8 * c, v + 8 * c);
+}
+
+// Same for half of the row: elements [0, HD/2) of `src` -> HD/4 columns at taddr.
+template <int HD>
+__device__ __forceinline__ void row_part_to_tmem(uint32_t taddr, const __nv_bfloat16* src, bool valid) {
+  constexpr int NC = HD / 4;  // 32-bit columns (bf16 pairs): 20 (hd 80) / 16 (hd 64) / 32 (hd 128)
+  uint32_t v[NC];
+#pragma unroll
+  for (int c = 0; c < NC / 4; ++c) {
+    const uint4 u = valid ? __ldg(reinterpret_cast<const uint4*>(src) + c) : make_uint4(0, 0, 0, 0);
+    v[4 * c] = u.x;
+    v[4 * c + 1] = u.y;
+    v[4 * c + 2] = u.z;
+    v[4 * c + 3] = u.w;
+  }
+#pragma unroll
+  for (int c = 0; c + 8 <= NC; c += 8) tc::tmem_st8(taddr + c, v + c);
+  if constexpr (NC % 8 == 4) tc::tmem_st4(taddr + NC - 4, v + NC - 4);
+}
+
 // dK/dV: one CTA per (128-key block, head), looping over 64-query blocks that
 // can see those keys: S^T = K Q_i^T and dP^T = V dO_i^T into TMEM; the softmax
-// warps form P^T = exp2(S^T*c - LSE) and dS^T = P^T (dP^T - delta) as bf16
-// over their S^T / dP^T columns in TMEM; dV += P^T dO_i and dK += dS^T Q_i
+// warps form P^T = exp2(S^T*c - LSE) and dS^T = P^T (dP^T - delta) and pack
+// both (bf16) into the S^T buffer they came from (P^T in the first, dS^T in the
+// second 16 columns of each 32-column half); dV += P^T dO_i and dK += dS^T Q_i
 // take A from TMEM and accumulate in TMEM. Each (key row, head) slice of the
 // fp32 dKV accumulator has exactly one owner CTA.
 template <int HD>
-__global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__ AttnBwdParams p) {
+__global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__ AttnBwdParams p) {
+  using C = DkvCfg<HD>;
   constexpr int QST = dkv_stages<HD>();
-  constexpr int KV_T = Lay<HD>::bytes(128), Q_T = Lay<HD>::bytes(64);
+  constexpr int NS = C::NS, ND = C::ND;
+  constexpr int KV_T = C::KVT ? 0 : Lay<HD>::bytes(128), Q_T = Lay<HD>::bytes(64);
+  static_assert(2 * 128 * HD * 4 <= 2 * KV_T + QST * (2 * Q_T + 512), "dK/dV epilogue staging must fit the ring");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sK = sm;
+  uint8_t* sK = sm;                 // (hd 128 only)
   uint8_t* sV = sK + KV_T;
   uint8_t* sQ = sV + KV_T;          // [QST]
   uint8_t* sdO = sQ + QST * Q_T;    // [QST]
-  float* sLD = reinterpret_cast<float*>(sdO + QST * Q_T);  // [QST][64 x (lse*log2e, delta)]
+  float* sLD = reinterpret_cast<float*>(sdO + QST * Q_T);  // [QST][-LSE*log2e x 64, -delta x 64]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + QST * 128);
-  uint64_t* kv_full = bars;
-  uint64_t* s_full = bars + 1;   // [2]
-  uint64_t* p_full = bars + 5;   // [2]
-  uint64_t* done = bars + 9;
-  uint64_t* q_full = bars + 10;          // [QST]
+  uint64_t* kv_full = bars;       // K/V resident (SMEM tiles, or TMEM copy)
+  uint64_t* done = bars + 1;
+  uint64_t* s_full = bars + 2;    // [NS]  S^T_i landed
+  uint64_t* sm_done = bars + 5;   // [NS]  P^T_i and dS^T_i packed into S buffer i % NS
+  uint64_t* dp_full = bars + 8;   // [ND]  dP^T_i landed
+  uint64_t* dp_free = bars + 10;  // [ND]  dP^T_i loaded into registers (buffer reusable)
+  uint64_t* q_full = bars + 12;          // [QST]
   uint64_t* q_empty = q_full + QST;      // [QST]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + QST);
+  uint64_t* s_free = q_empty + QST;      // [NS]  dV/dK_i completed: S buffer i % NS reusable
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + NS);
 
   // 2-CTA cluster: CTAs own adjacent 128-key blocks and stream the same query
   // blocks; each Q_i / dO_i tile is fetched once from L2 and multicast to both
@@ -470,7 +640,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
   const uint32_t rank = tc::cluster_ctarank();
   const int num_kb = static_cast<int>((p.kv_len + 127) / 128);
   const int num_kb2 = (num_kb + 1) & ~1;
-  const int kb = num_kb2 - 1 - static_cast<int>(blockIdx.x);  // heaviest first; may be == num_kb (idle keys)
+  const int kb = num_kb2 - 1 - static_cast<int>(blockIdx.x);  // may be == num_kb (idle keys)
   const int head = blockIdx.y;
   const int64_t j0 = static_cast<int64_t>(kb) * 128;
   const int64_t j0_lo = static_cast<int64_t>(num_kb2 - 2 - 2 * static_cast<int>(blockIdx.x / 2)) * 128;
@@ -480,174 +650,230 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
   const int niter = static_cast<int>((p.n - ib0 + 63) / 64);
 
   if (threadIdx.x == 0) {
-    tc::mbar_init(kv_full, 1);
+    tc::mbar_init(kv_full, C::KVT ? 16 : 1);  // softmax warps (TMEM copy) or the TMA
     tc::mbar_init(done, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&p_full[i], 256);
+      tc::mbar_init(&sm_done[i], 16);
+    }
+    for (int i = 0; i < ND; ++i) {
+      tc::mbar_init(&dp_full[i], 1);
+      tc::mbar_init(&dp_free[i], 16);
     }
     for (int i = 0; i < QST; ++i) {
       tc::mbar_init(&q_full[i], 1);
       tc::mbar_init(&q_empty[i], 2);  // freed by both CTAs' MMA commits
     }
+    for (int i = 0; i < NS; ++i) tc::mbar_init(&s_free[i], 1);
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
   tc::cluster_sync();
   tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // TMEM: S^T[2] at 0/64, dP^T[2] at 128/192, dV at 256, dK at 384. P^T and
-  // dS^T (bf16) overwrite the S^T / dP^T columns they were computed from.
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform (keeps MMA operands in uniform registers)
 
   if (warp == 0) {
     if (lane == 0) {
       tc::tma_prefetch(&p.tq.m0);
       tc::tma_prefetch(&p.tdo.m0);
-      tc::tma_prefetch(&p.tkv.m0);
-      tc::mbar_expect_tx(kv_full, 2 * KV_T);
-      load_tile<HD>(sK, p.tkv, kv_full, head * HD, static_cast<int>(j0), 128, 0);
-      load_tile<HD>(sV, p.tkv, kv_full, p.h + head * HD, static_cast<int>(j0), 128, 0);
+      if constexpr (!C::KVT) {
+        tc::tma_prefetch(&p.tkv.m0);
+        tc::mbar_expect_tx(kv_full, 2 * Lay<HD>::bytes(128));
+        load_tile<HD>(sK, p.tkv, kv_full, head * HD, static_cast<int>(j0), 128, 0);
+        load_tile<HD>(sV, p.tkv, kv_full, p.h + head * HD, static_cast<int>(j0), 128, 0);
+      }
       for (int it = 0; it < niter; ++it) {
         const int st = it % QST;
         const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
         tc::mbar_wait(&q_empty[st], ((it / QST) & 1) ^ 1);  // stage free in both CTAs
+        trace_mark(p, 0, it);
         tc::mbar_expect_tx(&q_full[st], 2 * Q_T + 512);
         if (rank == 0)
           load_tile<HD>(sQ + st * Q_T, p.tq, &q_full[st], head * HD, static_cast<int>(i0), 64, 3);
         else
           load_tile<HD>(sdO + st * Q_T, p.tdo, &q_full[st], head * HD, static_cast<int>(i0), 64, 3);
-        // (LSE*log2e, delta) pairs of the 64 queries: one async 512-byte bulk copy
+        // (-LSE*log2e, -delta) of the 64 queries: one async 512-byte bulk copy
         tc::bulk_load(sLD + st * 128, p.ld + (static_cast<int64_t>(head) * p.n_pad + i0) * 2, 512, &q_full[st]);
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = tc::idesc_bf16(128, 64, false, false);
-      tc::mbar_wait(kv_full, 0);
+  } else if (warp == 1 || warp == 2) {
+    // Two MMA-issuing warps (whole warp converged; tc::*_w elect the issuing
+    // lane). A tcgen05.mma issue returns only about when the tensor pipe takes
+    // it, so every cycle an issuing warp spends waiting on a barrier is a pipe
+    // bubble; with S/dP on warp 1 and dV/dK on warp 2, one warp's waits are
+    // covered by the other's issue. Cross-warp TMEM reuse is ordered by
+    // barriers (s_free: dV/dK_i completed), not by issue order.
+    constexpr uint32_t idesc_s = tc::idesc_bf16(128, 64, false, false);
+    tc::mbar_wait_w(kv_full, 0);
+    tc::tc_fence_after();
+    if (warp == 1) {
       const uint32_t k_base = tc::smem_u32(sK), v_base = tc::smem_u32(sV);
-      // Two independent issue queues polled without blocking: S^T/dP^T of block
-      // s_it (once dV/dK of block s_it-2, which read its TMEM buffer, have been
-      // issued: MMAs execute in issue order) and dV/dK of block g_it.
-      int s_it = 0, g_it = 0;
-      while (g_it < niter) {
-        if (s_it < niter && s_it < g_it + 2 && tc::mbar_test(&q_full[s_it % QST], (s_it / QST) & 1)) {
-          const int it = s_it++;
-          const int b = it & 1, st = it % QST;
-          tc::tc_fence_after();
-          const uint32_t q_base = tc::smem_u32(sQ + st * Q_T), do_base = tc::smem_u32(sdO + st * Q_T);
-          if (!(p.dbg & 1)) {
+      // S^T = K Q^T / dP^T = V dO^T: A = K / V (TMEM copy, or SMEM tile for hd 128).
+      auto kv_mma = [&](uint32_t d, uint32_t t_a, uint32_t a_base, uint32_t b_base) {
 #pragma unroll
-            for (int kk = 0; kk < HD / 16; ++kk) {
-              tc::mma_bf16_ss(tmem + b * 64, kdesc<HD>(k_base, 128, kk), kdesc<HD>(q_base, 64, kk), idesc_s, kk > 0);
-              tc::mma_bf16_ss(tmem + 128 + b * 64, kdesc<HD>(v_base, 128, kk), kdesc<HD>(do_base, 64, kk), idesc_s,
-                              kk > 0);
-            }
-          }
-          tc::mma_commit(&s_full[b]);
-          continue;
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          if constexpr (C::KVT)
+            tc::mma_bf16_ts_w(d, tmem + t_a + 8 * kk, kdesc<HD>(b_base, 64, kk), idesc_s, kk > 0);
+          else
+            tc::mma_bf16_ss_w(d, kdesc<HD>(a_base, 128, kk), kdesc<HD>(b_base, 64, kk), idesc_s, kk > 0);
         }
-        if (g_it < s_it && tc::mbar_test(&p_full[g_it & 1], (g_it >> 1) & 1)) {
-          const int it = g_it++;
-          const int b = it & 1, st = it % QST;
-          tc::tc_fence_after();
-          const uint32_t q_base = tc::smem_u32(sQ + st * Q_T), do_base = tc::smem_u32(sdO + st * Q_T);
-          if (!(p.dbg & 1)) {
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries
-              const bool acc = it > 0 || kk > 0;
-              mma_nhd_ts<HD>(tmem + 256, tmem + b * 64 + half_packed_col(kk), do_base, 64, kk, acc);
-              mma_nhd_ts<HD>(tmem + 384, tmem + 128 + b * 64 + half_packed_col(kk), q_base, 64, kk, acc);
-            }
-          }
-          tc::mma_commit_mc(&q_empty[st], 3);  // this CTA is done with the multicast stage
-        }
+      };
+      for (int it = 0; it < niter; ++it) {
+        const int b = it % NS, st = it % QST;
+        tc::mbar_wait_w(&q_full[st], (it / QST) & 1);
+        if (it >= NS) tc::mbar_wait_w(&s_free[b], ((it / NS) - 1) & 1);  // dV/dK of it-NS read buffer b
+        tc::tc_fence_after();
+        if (!(p.dbg & 1)) kv_mma(tmem + b * 64, C::T_K, k_base, tc::smem_u32(sQ + st * Q_T));
+        tc::mma_commit_w(&s_full[b]);
+        trace_mark(p, 3, it);
+        if (it >= ND) tc::mbar_wait_w(&dp_free[it % ND], ((it / ND) - 1) & 1);  // softmax loaded dP^T_{it-ND}
+        tc::tc_fence_after();
+        if (!(p.dbg & 1)) kv_mma(tmem + C::T_DP + (it % ND) * 64, C::T_V, v_base, tc::smem_u32(sdO + st * Q_T));
+        tc::mma_commit_w(&dp_full[it % ND]);
+        trace_mark(p, 2, it);
       }
-      tc::mma_commit(done);
+    } else {
+      for (int it = 0; it < niter; ++it) {
+        const int b = it % NS, st = it % QST;
+        tc::mbar_wait_w(&sm_done[b], (it / NS) & 1);
+        tc::tc_fence_after();
+        const uint32_t q_base = tc::smem_u32(sQ + st * Q_T), do_base = tc::smem_u32(sdO + st * Q_T);
+        if (!(p.dbg & 1)) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries
+            const bool acc = it > 0 || kk > 0;
+            const uint32_t col = b * 64 + 16 * kk;  // softmax group kk packed P^T | dS^T here
+            mma_nhd_ts<HD>(tmem + C::T_DV, tmem + col, do_base, 64, kk, acc);
+            mma_nhd_ts<HD>(tmem + C::T_DK, tmem + col + 8, q_base, 64, kk, acc);
+          }
+        }
+        tc::mma_commit_mc_w(&q_empty[st], 3);  // this CTA is done with the multicast stage
+        tc::mma_commit_w(&s_free[b]);
+        trace_mark(p, 1, it);
+      }
+      tc::mma_commit_w(done);
     }
   } else if (warp >= 4) {
-    // 8 softmax warps: warps w and w+4 share TMEM lane quarter w%4 (one key row
-    // per lane) and split the 64 query columns in halves -> two warps per SMSP.
-    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    // 16 softmax warps: warp w reads TMEM lane quarter w%4 (one key row per
+    // lane) and query columns [16g, 16g+16) of each 64-query block, g = (w-4)/4:
+    // four warps per SMSP hide the TMEM-load / MUFU / barrier latencies.
+    const int quarter = warp & 3, g = (warp - 4) >> 2;
     const int r = quarter * 32 + lane;  // key row
     const int64_t kpos = j0 + r;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    for (int it = 0; it < niter; ++it) {
-      const int b = it & 1, st = it % QST;
-      const uint32_t ph = (it >> 1) & 1;
-      const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
-      const float* ld = sLD + st * 128 + half * 64;  // this half's 32 (lse, delta) pairs
-      tc::mbar_wait(&q_full[st], (it / QST) & 1);    // LSE / delta of this block are in SMEM
-      // visible query columns c (local to this half): q_off + i0 + 32*half + c >= kpos, i0 + 32*half + c < n
-      const int64_t cbase = i0 + half * 32;
-      int64_t cmin = kpos - p.q_off - cbase;
-      const int c_lo = cmin < 0 ? 0 : (cmin > 32 ? 32 : static_cast<int>(cmin));
-      const int64_t chi = p.n - cbase;
-      const int c_hi = chi < 0 ? 0 : (chi > 32 ? 32 : static_cast<int>(chi));  // exclusive
-      tc::mbar_wait(&s_full[b], ph);
-      tc::tc_fence_after();
-      uint32_t sv[32], dpv[32];
-      tc::tmem_ld32(tmem + lane_base + b * 64 + half * 32, sv);
-      tc::tmem_ld32(tmem + lane_base + 128 + b * 64 + half * 32, dpv);
-      tc::tmem_ld_wait();
-      const bool full_blk = __all_sync(0xffffffffu, c_lo == 0 && c_hi == 32);
-      uint32_t wp[16], wd[16];
-#pragma unroll
-      for (int e = 0; e < 32; e += 4) {
-        if (p.dbg & 2) break;
-        const float4 a4 = lds_f4(ld + 2 * e);      // (lse, delta) of queries e, e+1 (warp broadcast)
-        const float4 b4 = lds_f4(ld + 2 * e + 4);  // (lse, delta) of queries e+2, e+3
-        const float lv[4] = {a4.x, a4.z, b4.x, b4.z}, dl[4] = {a4.y, a4.w, b4.y, b4.w};
-        float pv[4], dv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int c = e + u;
-          float pr = ex2(fmaf(__uint_as_float(sv[c]), p.scale_log2, -lv[u]));
-          if (!full_blk && (c < c_lo || c >= c_hi)) pr = 0.f;
-          pv[u] = pr;
-          dv[u] = pr * (__uint_as_float(dpv[c]) - dl[u]);
-        }
-        wp[e / 2] = pack_bf16(pv[0], pv[1]);
-        wp[e / 2 + 1] = pack_bf16(pv[2], pv[3]);
-        wd[e / 2] = pack_bf16(dv[0], dv[1]);
-        wd[e / 2 + 1] = pack_bf16(dv[2], dv[3]);
-      }
-      tc::tmem_st16(tmem + lane_base + b * 64 + half * 32, wp);
-      tc::tmem_st16(tmem + lane_base + 128 + b * 64 + half * 32, wd);
+    if constexpr (C::KVT) {  // groups 0/1 copy halves of this lane's K row, groups 2/3 of its V row
+      const bool kv_ok = kpos < p.kv_len;
+      const int part = g & 1;
+      row_part_to_tmem<HD>(tmem + lane_base + (g >= 2 ? C::T_V : C::T_K) + part * (HD / 4),
+                           p.kv + (kv_ok ? kpos : 0) * 2 * p.h + (g >= 2 ? p.h : 0) + head * HD + part * (HD / 2),
+                           kv_ok);
       tc::tmem_st_wait();
       tc::tc_fence_before();
-      tc::mbar_arrive(&p_full[b]);
+      warp_arrive(kv_full);
+    }
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+    for (int it = 0; it < niter; ++it) {
+      const int b = it % NS, st = it % QST, d = it % ND;
+      const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
+      const float* nl = sLD + st * 128 + g * 16;  // -LSE*log2e of this group's 16 queries
+      const float* nd = nl + 64;                  // -delta of the same queries
+      // visible query columns c (local): q_off + i0 + 16g + c >= kpos, i0 + 16g + c < n
+      const int64_t cbase = i0 + g * 16;
+      const int64_t cmin = kpos - p.q_off - cbase;
+      const int c_lo = cmin < 0 ? 0 : (cmin > 16 ? 16 : static_cast<int>(cmin));
+      const int64_t chi = p.n - cbase;
+      const int c_hi = chi < 0 ? 0 : (chi > 16 ? 16 : static_cast<int>(chi));  // exclusive
+      const bool full_blk = __all_sync(0xffffffffu, c_lo == 0 && c_hi == 16);
+      tc::mbar_wait(&q_full[st], (it / QST) & 1);  // LSE / delta of this block are in SMEM
+      if (warp == 4) trace_mark(p, 4, it);
+      uint32_t sv[16], dpv[16];
+      tc::mbar_wait(&s_full[b], (it / NS) & 1);
+      if (warp == 4) trace_mark(p, 5, it);
+      if (p.dbg & 2) {  // protocol only
+        tc::mbar_wait(&dp_full[d], (it / ND) & 1);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&dp_free[d]);
+        warp_arrive(&sm_done[b]);
+        continue;
+      }
+      tc::tc_fence_after();
+      tmem_ld16(tmem + lane_base + b * 64 + g * 16, sv);
+      tc::mbar_wait(&dp_full[d], (it / ND) & 1);
+      if (warp == 4) trace_mark(p, 6, it);
+      tc::tc_fence_after();
+      tmem_ld16(tmem + lane_base + C::T_DP + d * 64 + g * 16, dpv);
+      tc::tmem_ld_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&dp_free[d]);  // the next dP MMA may overwrite the buffer
+      uint32_t wp[8], wd[8];
+      // P^T = exp2(S^T*c - LSE), dS^T = P^T (dP^T - delta): packed FFMA2 / FADD2 / FMUL2;
+      // the mask is only evaluated on blocks that touch the diagonal or the end.
+      auto body = [&](auto masked) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) {
+          const float4 l4 = lds_f4(nl + e), d4 = lds_f4(nd + e);  // warp broadcast
+          const bool poly = bwd_poly_group(2 * (e / 4));
+          float2 p0 = ex2x2_sel(poly, ffma2(u2f2(sv[e], sv[e + 1]), sc2, make_float2(l4.x, l4.y)));
+          float2 p1 = ex2x2_sel(poly, ffma2(u2f2(sv[e + 2], sv[e + 3]), sc2, make_float2(l4.z, l4.w)));
+          if constexpr (decltype(masked)::value) {
+            if (e < c_lo || e >= c_hi) p0.x = 0.f;
+            if (e + 1 < c_lo || e + 1 >= c_hi) p0.y = 0.f;
+            if (e + 2 < c_lo || e + 2 >= c_hi) p1.x = 0.f;
+            if (e + 3 < c_lo || e + 3 >= c_hi) p1.y = 0.f;
+          }
+          const float2 g0 = fmul2(p0, fadd2(u2f2(dpv[e], dpv[e + 1]), make_float2(d4.x, d4.y)));
+          const float2 g1 = fmul2(p1, fadd2(u2f2(dpv[e + 2], dpv[e + 3]), make_float2(d4.z, d4.w)));
+          wp[e / 2] = pack2(p0);
+          wp[e / 2 + 1] = pack2(p1);
+          wd[e / 2] = pack2(g0);
+          wd[e / 2 + 1] = pack2(g1);
+        }
+      };
+      if (full_blk)
+        body(std::false_type{});
+      else
+        body(std::true_type{});
+      tc::tmem_st8(tmem + lane_base + b * 64 + g * 16, wp);      // P^T  -> columns [16g, 16g+8)
+      tc::tmem_st8(tmem + lane_base + b * 64 + g * 16 + 8, wd);  // dS^T -> columns [16g+8, 16g+16)
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      warp_arrive(&sm_done[b]);
+      if (warp == 4) trace_mark(p, 7, it);
     }
     tc::mbar_wait(done, 0);
     tc::tc_fence_after();
-    const bool own = kpos < p.kv_len;
-    float* dk_row = p.dkv + (own ? kpos : 0) * 2 * p.h + head * HD;
-    float* dv_row = dk_row + p.h;
-    constexpr int NCH = HD / 16, SPLIT = (NCH + 1) / 2;
-    for (int c = half ? SPLIT : 0; c < (half ? NCH : SPLIT); ++c) {
-      uint32_t v[16], k[16];
-      // tcgen05.ld is warp-collective: every lane loads, only owners store.
-      tmem_ld16(tmem + lane_base + 256 + c * 16, v);
-      tmem_ld16(tmem + lane_base + 384 + c * 16, k);
+    if (warp == 4) trace_mark(p, 8, 0);
+    // Epilogue: dK (scaled) / dV rows -> SMEM [2][128][HD] fp32 (the Q/dO ring is
+    // idle: every MMA completed and every multicast stage was consumed), then one
+    // thread adds both tiles into the fp32 accumulator with TMA reduce-add
+    // (coalesced, asynchronous in L2; rows >= kv_len are clipped by the map).
+    float* out = reinterpret_cast<float*>(sm);
+    constexpr int NCH = HD / 16;
+    for (int t = g; t < 2 * NCH; t += 4) {  // 16-column chunks of dV (t < NCH) then dK
+      const bool is_k = t >= NCH;
+      const int c = is_k ? t - NCH : t;
+      uint32_t v[16];
+      tmem_ld16(tmem + lane_base + (is_k ? C::T_DK : C::T_DV) + c * 16, v);
       tc::tmem_ld_wait();
-      if (own) {
+      const float sc = is_k ? p.scale : 1.f;
+      float* dst = out + (is_k ? 0 : 128 * HD) + r * HD + c * 16;
 #pragma unroll
-        for (int e = 0; e < 16; e += 4) {
-          float4 a = *reinterpret_cast<float4*>(dv_row + c * 16 + e);
-          a.x += __uint_as_float(v[e]);
-          a.y += __uint_as_float(v[e + 1]);
-          a.z += __uint_as_float(v[e + 2]);
-          a.w += __uint_as_float(v[e + 3]);
-          *reinterpret_cast<float4*>(dv_row + c * 16 + e) = a;
-          float4 g = *reinterpret_cast<float4*>(dk_row + c * 16 + e);
-          g.x += __uint_as_float(k[e]) * p.scale;
-          g.y += __uint_as_float(k[e + 1]) * p.scale;
-          g.z += __uint_as_float(k[e + 2]) * p.scale;
-          g.w += __uint_as_float(k[e + 3]) * p.scale;
-          *reinterpret_cast<float4*>(dk_row + c * 16 + e) = g;
-        }
-      }
+      for (int e = 0; e < 16; e += 4)
+        *reinterpret_cast<float4*>(dst + e) =
+            make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
+                        __uint_as_float(v[e + 3]) * sc);
     }
+    tc::fence_proxy_async_smem();
+    tc::named_bar_sync(1, 512);
+    if (warp == 4 && lane == 0) {
+      tc::tma_reduce_add_2d(&p.tdkv, out, head * HD, static_cast<int>(j0));
+      tc::tma_reduce_add_2d(&p.tdkv, out + 128 * HD, p.h + head * HD, static_cast<int>(j0));
+      tc::bulk_commit();
+      tc::bulk_wait_read0();  // SMEM must outlive the copy-out
+    }
+    if (warp == 4) trace_mark(p, 9, 0);
   }
   tc::tc_fence_before();
   tc::cluster_sync();  // no multicast data / remote arrive may target an exited CTA
@@ -656,26 +882,30 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_k(const __grid_constant__
 }
 
 // dQ: one CTA per (128-query block, head), looping over 64-key blocks:
-// S = Q K_j^T, dP = dO V_j^T; dS = P (dP - delta) (bf16, over the dP columns
-// in TMEM); dQ += dS K_j with A from TMEM.
+// S = Q K_j^T, dP = dO V_j^T (A = Q / dO copied into TMEM once); dS = P (dP -
+// delta) is packed (bf16) into the S buffer it came from; dQ += dS K_j with A
+// from TMEM.
 template <int HD>
-__global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ AttnBwdParams p) {
+__global__ void __launch_bounds__(640, 1) attn_bwd_dq_k(const __grid_constant__ AttnBwdParams p) {
+  using C = DqCfg<HD>;
   constexpr int KST = dq_stages<HD>();
-  constexpr int Q_T = Lay<HD>::bytes(128), K_T = Lay<HD>::bytes(64);
+  constexpr int NS = C::NS, ND = C::ND;
+  constexpr int K_T = Lay<HD>::bytes(64);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;
-  uint8_t* sdO = sQ + Q_T;
-  uint8_t* sK = sdO + Q_T;        // [KST]
+  uint8_t* sK = sm;               // [KST]
   uint8_t* sV = sK + KST * K_T;   // [KST]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + KST * K_T);
-  uint64_t* qo_full = bars;
-  uint64_t* s_full = bars + 1;    // [2]
-  uint64_t* ds_full = bars + 5;   // [2]
-  uint64_t* done = bars + 9;
-  uint64_t* kv_full = bars + 10;       // [KST]
+  uint64_t* qo_full = bars;       // Q, dO copied into TMEM
+  uint64_t* done = bars + 1;
+  uint64_t* s_full = bars + 2;    // [NS]
+  uint64_t* ds_full = bars + 5;   // [NS]
+  uint64_t* dp_full = bars + 8;   // [ND]
+  uint64_t* dp_free = bars + 10;  // [ND]
+  uint64_t* kv_full = bars + 12;       // [KST]
   uint64_t* kv_empty = kv_full + KST;  // [KST]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + KST);
+  uint64_t* s_free = kv_empty + KST;   // [NS]  dQ_j completed: score buffer j % NS reusable
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + NS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int num_qb = static_cast<int>((p.n + 127) / 128);
@@ -687,33 +917,32 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ 
   const int nblk = static_cast<int>((kend + 63) / 64);
 
   if (threadIdx.x == 0) {
-    tc::mbar_init(qo_full, 1);
+    tc::mbar_init(qo_full, 16);
     tc::mbar_init(done, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&ds_full[i], 256);
+      tc::mbar_init(&ds_full[i], 16);
+    }
+    for (int i = 0; i < ND; ++i) {
+      tc::mbar_init(&dp_full[i], 1);
+      tc::mbar_init(&dp_free[i], 16);
     }
     for (int i = 0; i < KST; ++i) {
       tc::mbar_init(&kv_full[i], 1);
       tc::mbar_init(&kv_empty[i], 1);
     }
+    for (int i = 0; i < NS; ++i) tc::mbar_init(&s_free[i], 1);
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // TMEM: S[2] at 0/64, dP[2] at 128/192 (dS overwrites dP), dQ at 256.
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform (keeps MMA operands in uniform registers)
 
   if (warp == 0) {
     if (lane == 0) {
-      tc::tma_prefetch(&p.tq.m0);
-      tc::tma_prefetch(&p.tdo.m0);
       tc::tma_prefetch(&p.tkv.m0);
-      tc::mbar_expect_tx(qo_full, 2 * Q_T);
-      load_tile<HD>(sQ, p.tq, qo_full, head * HD, static_cast<int>(q0), 128, 0);
-      load_tile<HD>(sdO, p.tdo, qo_full, head * HD, static_cast<int>(q0), 128, 0);
       for (int j = 0; j < nblk; ++j) {
         const int st = j % KST;
         tc::mbar_wait(&kv_empty[st], ((j / KST) & 1) ^ 1);
@@ -722,91 +951,111 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ 
         load_tile<HD>(sV + st * K_T, p.tkv, &kv_full[st], p.h + head * HD, j * 64, 64, 0);
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = tc::idesc_bf16(128, 64, false, false);
-      tc::mbar_wait(qo_full, 0);
-      const uint32_t q_base = tc::smem_u32(sQ), do_base = tc::smem_u32(sdO);
-      // Polled issue queues: S/dP of block sj (once dQ of block sj-2, which
-      // reads dS from the same TMEM buffer, is issued) and dQ += dS K of block gj.
-      int sj = 0, gj = 0;
-      while (gj < nblk) {
-        if (sj < nblk && sj < gj + 2 && tc::mbar_test(&kv_full[sj % KST], (sj / KST) & 1)) {
-          const int j = sj++;
-          const int b = j & 1, st = j % KST;
-          tc::tc_fence_after();
-          const uint32_t k_base = tc::smem_u32(sK + st * K_T), v_base = tc::smem_u32(sV + st * K_T);
+  } else if (warp == 1 || warp == 2) {
+    // Two MMA-issuing warps (see the dK/dV kernel): warp 1 issues S_j / dP_j,
+    // warp 2 issues dQ += dS_j K_j; score-buffer reuse is ordered by s_free.
+    constexpr uint32_t idesc_s = tc::idesc_bf16(128, 64, false, false);
+    tc::mbar_wait_w(qo_full, 0);
+    tc::tc_fence_after();
+    if (warp == 1) {
+      for (int j = 0; j < nblk; ++j) {
+        const int b = j % NS, st = j % KST;
+        tc::mbar_wait_w(&kv_full[st], (j / KST) & 1);
+        if (j >= NS) tc::mbar_wait_w(&s_free[b], ((j / NS) - 1) & 1);  // dQ_{j-NS} read buffer b
+        tc::tc_fence_after();
+        const uint32_t k_base = tc::smem_u32(sK + st * K_T), v_base = tc::smem_u32(sV + st * K_T);
 #pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            tc::mma_bf16_ss(tmem + b * 64, kdesc<HD>(q_base, 128, kk), kdesc<HD>(k_base, 64, kk), idesc_s, kk > 0);
-            tc::mma_bf16_ss(tmem + 128 + b * 64, kdesc<HD>(do_base, 128, kk), kdesc<HD>(v_base, 64, kk), idesc_s,
+        for (int kk = 0; kk < HD / 16; ++kk)
+          tc::mma_bf16_ts_w(tmem + b * 64, tmem + C::T_Q + 8 * kk, kdesc<HD>(k_base, 64, kk), idesc_s, kk > 0);
+        tc::mma_commit_w(&s_full[b]);
+        if (j >= ND) tc::mbar_wait_w(&dp_free[j % ND], ((j / ND) - 1) & 1);  // softmax loaded dP_{j-ND}
+        tc::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          tc::mma_bf16_ts_w(tmem + C::T_DP + (j % ND) * 64, tmem + C::T_DO + 8 * kk, kdesc<HD>(v_base, 64, kk), idesc_s,
                             kk > 0);
-          }
-          tc::mma_commit(&s_full[b]);
-          continue;
-        }
-        if (gj < sj && tc::mbar_test(&ds_full[gj & 1], (gj >> 1) & 1)) {
-          const int j = gj++;
-          const int b = j & 1, st = j % KST;
-          tc::tc_fence_after();
-          const uint32_t k_base = tc::smem_u32(sK + st * K_T);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // K = 64 keys
-            mma_nhd_ts<HD>(tmem + 256, tmem + 128 + b * 64 + half_packed_col(kk), k_base, 64, kk, j > 0 || kk > 0);
-          tc::mma_commit(&kv_empty[st]);
-        }
+        tc::mma_commit_w(&dp_full[j % ND]);
       }
-      tc::mma_commit(done);
+    } else {
+      for (int j = 0; j < nblk; ++j) {
+        const int b = j % NS, st = j % KST;
+        tc::mbar_wait_w(&ds_full[b], (j / NS) & 1);
+        tc::tc_fence_after();
+        const uint32_t k_base = tc::smem_u32(sK + st * K_T);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // K = 64 keys
+          mma_nhd_ts<HD>(tmem + C::T_DQ, tmem + b * 64 + 16 * kk, k_base, 64, kk, j > 0 || kk > 0);
+        tc::mma_commit_w(&kv_empty[st]);  // S_j / dP_j (also readers of the stage) completed before dS_j
+        tc::mma_commit_w(&s_free[b]);
+      }
+      tc::mma_commit_w(done);
     }
   } else if (warp >= 4) {
-    // 8 softmax warps: warps w and w+4 share lane quarter w%4 (one query row per
-    // lane) and split the 64 key columns of each block in halves.
-    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    // 16 softmax warps: warp w reads lane quarter w%4 (one query row per lane)
+    // and key columns [16g, 16g+16) of each 64-key block, g = (w-4)/4.
+    const int quarter = warp & 3, g = (warp - 4) >> 2;
     const int r = quarter * 32 + lane;
     const int64_t row = q0 + r;
     const bool valid = row < p.n;
     const int64_t qpos = p.q_off + row;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    const float2 ldv = *reinterpret_cast<const float2*>(p.ld + (static_cast<int64_t>(head) * p.n_pad + row) * 2);
-    const float lse2 = ldv.x, dlt = ldv.y;  // zero-padded past n
-    for (int j = 0; j < nblk; ++j) {
-      const int b = j & 1;
-      const uint32_t ph = (j >> 1) & 1;
-      // key columns c (local to this half) with j*64 + 32*half + c <= qpos are visible
-      const int64_t lim64 = valid ? qpos - static_cast<int64_t>(j) * 64 - half * 32 : -1;
-      const int lim = lim64 > 1000 ? 1000 : static_cast<int>(lim64);
-      tc::mbar_wait(&s_full[b], ph);
-      tc::tc_fence_after();
-      uint32_t sv[32], dpv[32];
-      tc::tmem_ld32(tmem + lane_base + b * 64 + half * 32, sv);
-      tc::tmem_ld32(tmem + lane_base + 128 + b * 64 + half * 32, dpv);
-      tc::tmem_ld_wait();
-      const bool full_blk = __all_sync(0xffffffffu, lim >= 31);
-      uint32_t w[16];
-#pragma unroll
-      for (int e = 0; e < 32; e += 2) {
-        float d2[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int c = e + u;
-          float pr = ex2(fmaf(__uint_as_float(sv[c]), p.scale_log2, -lse2));
-          if (!full_blk && c > lim) pr = 0.f;
-          d2[u] = pr * (__uint_as_float(dpv[c]) - dlt);
-        }
-        w[e / 2] = pack_bf16(d2[0], d2[1]);
-      }
-      tc::tmem_st16(tmem + lane_base + 128 + b * 64 + half * 32, w);
+    {  // groups 0/1 copy halves of this lane's Q row into TMEM, groups 2/3 of its dO row
+      const int part = g & 1;
+      row_part_to_tmem<HD>(tmem + lane_base + (g >= 2 ? C::T_DO : C::T_Q) + part * (HD / 4),
+                           (g >= 2 ? p.dout : p.q) + (valid ? row : 0) * p.h + head * HD + part * (HD / 2), valid);
       tc::tmem_st_wait();
       tc::tc_fence_before();
-      tc::mbar_arrive(&ds_full[b]);
+      warp_arrive(qo_full);
+    }
+    // (-LSE*log2e, -delta) of this query row (zero padded past n): blocks of 64 queries.
+    const int64_t ldi = (static_cast<int64_t>(head) * p.n_pad + (row & ~int64_t(63))) * 2 + (row & 63);
+    const float2 nl2 = make_float2(p.ld[ldi], p.ld[ldi]), nd2 = make_float2(p.ld[ldi + 64], p.ld[ldi + 64]);
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+    for (int j = 0; j < nblk; ++j) {
+      const int b = j % NS, d = j % ND;
+      // key columns c (local) with j*64 + 16g + c <= qpos are visible
+      const int64_t lim64 = valid ? qpos - static_cast<int64_t>(j) * 64 - g * 16 : -1;
+      const int lim = lim64 > 1000 ? 1000 : static_cast<int>(lim64);
+      const bool full_blk = __all_sync(0xffffffffu, lim >= 15);
+      uint32_t sv[16], dpv[16];
+      tc::mbar_wait(&s_full[b], (j / NS) & 1);
+      tc::tc_fence_after();
+      tmem_ld16(tmem + lane_base + b * 64 + g * 16, sv);
+      tc::mbar_wait(&dp_full[d], (j / ND) & 1);
+      tc::tc_fence_after();
+      tmem_ld16(tmem + lane_base + C::T_DP + d * 64 + g * 16, dpv);
+      tc::tmem_ld_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&dp_free[d]);
+      uint32_t w[8];
+      auto body = [&](auto masked) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          float2 pr = ex2x2_sel(dq_poly_group(e / 2), ffma2(u2f2(sv[e], sv[e + 1]), sc2, nl2));
+          if constexpr (decltype(masked)::value) {
+            if (e > lim) pr.x = 0.f;
+            if (e + 1 > lim) pr.y = 0.f;
+          }
+          w[e / 2] = pack2(fmul2(pr, fadd2(u2f2(dpv[e], dpv[e + 1]), nd2)));
+        }
+      };
+      if (full_blk)
+        body(std::false_type{});
+      else
+        body(std::true_type{});
+      tc::tmem_st8(tmem + lane_base + b * 64 + g * 16, w);  // dS -> columns [16g, 16g+8) of the S buffer
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      warp_arrive(&ds_full[b]);
     }
     tc::mbar_wait(done, 0);
     tc::tc_fence_after();
     __nv_bfloat16* dq_row = p.dq + (valid ? row : 0) * p.h + head * HD;
-    constexpr int NCH = HD / 16, SPLIT = (NCH + 1) / 2;
-    for (int c = half ? SPLIT : 0; c < (half ? NCH : SPLIT); ++c) {
+    constexpr int NCH = HD / 16;
+    for (int c = g; c < NCH; c += 4) {
       uint32_t v[16];
-      tmem_ld16(tmem + lane_base + 256 + c * 16, v);  // warp-collective: all lanes
+      tmem_ld16(tmem + lane_base + C::T_DQ + c * 16, v);  // warp-collective: all lanes
       tc::tmem_ld_wait();
       if (!valid) continue;
       uint4 u0 = make_uint4(pack_bf16(__uint_as_float(v[0]) * p.scale, __uint_as_float(v[1]) * p.scale),
@@ -827,8 +1076,9 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_k(const __grid_constant__ 
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-// ld[head][i] = (lse * log2e, sum_d dO*O) for i < n, zeros up to n_pad: the
-// per-query vectors the backward kernels stream (one warp per (i, head)).
+// ld: per head, blocks of 64 queries laid out as [64 x -LSE*log2e][64 x -delta],
+// delta = sum_d dO*O; zeros up to n_pad. One warp per (i, head). The dK/dV
+// kernel bulk-copies one 512-byte block per 64-query step.
 __global__ void attn_prep_k(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                             const float* __restrict__ lse, float* __restrict__ ld, int64_t n, int64_t n_pad, int H,
                             int hd) {
@@ -844,7 +1094,11 @@ __global__ void attn_prep_k(const __nv_bfloat16* __restrict__ o, const __nv_bflo
     d = warp_sum(d);
     l = lse[(int64_t)head * n + i] * 1.4426950408889634f;
   }
-  if (lane == 0) *reinterpret_cast<float2*>(ld + (head * n_pad + i) * 2) = make_float2(l, d);
+  if (lane == 0) {
+    const int64_t at = (head * n_pad + (i & ~int64_t(63))) * 2 + (i & 63);
+    ld[at] = -l;
+    ld[at + 64] = -d;
+  }
 }
 
 // ---------------------------------------------------------------------------- host
@@ -907,7 +1161,7 @@ void attn_fwd_tc(const void* q, const void* kv, void* o, float* lse, int64_t n, 
   }
 }
 
-size_t attn_bwd_ws_delta_floats(int64_t n, int H) { return static_cast<size_t>(H) * ((n + 63) / 64 * 64) * 2; }
+size_t attn_bwd_ws_delta_floats(int64_t n, int H) { return static_cast<size_t>(H) * ((n + 127) / 128 * 128) * 2; }
 
 void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout, const float* lse, float* ws_delta,
                  float* ws_dq, void* dq, float* dkv, int64_t n, int64_t q_off, int64_t kv_len, int H, int hd,
@@ -917,7 +1171,7 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
        reinterpret_cast<uintptr_t>(dq) | reinterpret_cast<uintptr_t>(dkv)) & 15)
     throw std::invalid_argument("attention: operands must be 16-byte aligned");
   (void)ws_dq;
-  const int64_t n_pad = (n + 63) / 64 * 64;
+  const int64_t n_pad = (n + 127) / 128 * 128;  // the dQ kernel reads whole 128-row blocks
   {
     const int64_t warps = n_pad * H;
     attn_prep_k<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(
@@ -933,6 +1187,19 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
   a.n_pad = n_pad;
   a.dkv = dkv;
   a.dq = static_cast<__nv_bfloat16*>(dq);
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * h), static_cast<cuuint64_t>(kv_len)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * h) * 4};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(hd), 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = tma_encode_fn()(&a.tdkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dkv, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (dkv) failed: " + std::to_string((int)r));
+  }
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.dout = static_cast<const __nv_bfloat16*>(dout);
+  a.kv = static_cast<const __nv_bfloat16*>(kv);
   a.n = n;
   a.q_off = q_off;
   a.kv_len = kv_len;
@@ -945,9 +1212,15 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
     return e ? std::atoi(e) : 0;
   }();
   a.dbg = dbg;
-  AttnBwdParams b = a;
-  make_maps(&b.tq, q, h, n, hd, 128);
-  make_maps(&b.tdo, dout, h, n, hd, 128);
+  static unsigned long long* trace_buf = [] {
+    unsigned long long* t = nullptr;
+    if (std::getenv("SP_ATTN_TRACE")) SPK_CUDA(cudaMalloc(&t, 16 * 64 * sizeof(unsigned long long)));
+    return t;
+  }();
+  a.trace = trace_buf;
+  if (trace_buf) SPK_CUDA(cudaMemsetAsync(trace_buf, 0, 16 * 64 * sizeof(unsigned long long), s));
+  AttnBwdParams b = a;  // dQ kernel: K/V in 64-row tiles (Q / dO go to TMEM from the raw rows)
+  b.trace = nullptr;
   make_maps(&b.tkv, kv, 2 * h, kv_len, hd, 64);
   auto run = [&](auto hd_tag) {
     constexpr int HD = decltype(hd_tag)::value;
@@ -959,7 +1232,7 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
       const unsigned nkb2 = static_cast<unsigned>(((kv_len + 127) / 128 + 1) & ~int64_t(1));
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3(nkb2, static_cast<unsigned>(H));
-      lc.blockDim = dim3(384);
+      lc.blockDim = dim3(640);
       lc.dynamicSmemBytes = smem_dkv;
       lc.stream = s;
       cudaLaunchAttribute at[1];
@@ -970,9 +1243,25 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
       lc.attrs = at;
       lc.numAttrs = 1;
       SPK_CUDA(cudaLaunchKernelEx(&lc, attn_bwd_dkv_k<HD>, a));
+      if (trace_buf) {
+        unsigned long long h_t[16 * 64];
+        SPK_CUDA(cudaMemcpyAsync(h_t, trace_buf, sizeof(h_t), cudaMemcpyDeviceToHost, s));
+        SPK_CUDA(cudaStreamSynchronize(s));
+        unsigned long long t0 = ~0ULL;
+        for (unsigned long long v : h_t)
+          if (v && v < t0) t0 = v;
+        std::fprintf(stderr, "dkv trace (cycles from first stamp): it q_load g_issue dp_issue s_issue sm_qfull sm_s sm_dp sm_done\n");
+        std::fprintf(stderr, "epilogue start %lld end %lld\n", (long long)(h_t[8 * 64] - t0), (long long)(h_t[9 * 64] - t0));
+        for (int it = 0; it < 64; ++it) {
+          std::fprintf(stderr, "%3d", it);
+          for (int e = 0; e < 8; ++e)
+            std::fprintf(stderr, " %8lld", h_t[e * 64 + it] ? (long long)(h_t[e * 64 + it] - t0) : -1LL);
+          std::fprintf(stderr, "\n");
+        }
+      }
     }
     dim3 g2(static_cast<unsigned>((n + 127) / 128), static_cast<unsigned>(H));
-    attn_bwd_dq_k<HD><<<g2, 384, smem_dq, s>>>(b);
+    attn_bwd_dq_k<HD><<<g2, 640, smem_dq, s>>>(b);
     SPK_LAUNCH_CHECK();
   };
   switch (hd) {

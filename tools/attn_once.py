@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """One forward + one backward of the tcgen05 prefix attention at the cfg-2 last-segment
-shape (n 6674 over a 32768-key prefix, 32 heads x 80) — the ncu capture target."""
+shape (n 6674 over a 32768-key prefix, 32 heads x 80) — the ncu capture target.
+Prints CUDA-event times of a second (warm) fwd and bwd."""
 import ctypes as C
 import sys
 from pathlib import Path
@@ -19,8 +20,14 @@ dq = torch.empty_like(q)
 dkv = torch.zeros(L, 2 * h, device="cuda")
 lib = _capi.lib()
 P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+s = torch.cuda.current_stream().cuda_stream
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 for _ in range(2):
-    _capi.check(lib.sp_attention_fwd(1, 0, P(q), P(kv), P(o), P(lse), n, q_off, L, H, hd, None))
-    _capi.check(lib.sp_attention_bwd(1, 0, P(q), P(kv), P(o), P(dout), P(lse), P(dq), P(dkv), n, q_off, L, H, hd, None))
+    ev[0].record()
+    _capi.check(lib.sp_attention_fwd(1, 0, P(q), P(kv), P(o), P(lse), n, q_off, L, H, hd, C.c_void_p(s)))
+    ev[1].record()
+    _capi.check(lib.sp_attention_bwd(1, 0, P(q), P(kv), P(o), P(dout), P(lse), P(dq), P(dkv), n, q_off, L, H, hd,
+                                     C.c_void_p(s)))
+    ev[2].record()
 torch.cuda.synchronize()
-print("ok")
+print(f"fwd {ev[0].elapsed_time(ev[1]):.3f} ms  bwd {ev[1].elapsed_time(ev[2]):.3f} ms")
