@@ -328,6 +328,20 @@ int sp_attention_fwd(int32_t dtype, int32_t impl, const void* q, const void* kv,
 int sp_attention_bwd(int32_t dtype, int32_t impl, const void* q, const void* kv, const void* o,
                      const void* dout, const float* lse, void* dq, float* dkv_acc, int64_t n,
                      int64_t q_off, int64_t kv_len, int32_t heads, int32_t head_dim, void* stream);
+/* Row norm of x [n, h] (LayerNorm, or RMSNorm when rms != 0) with gain g [h] fp32; saves
+ * mean (LayerNorm only) and rstd [n] fp32. Backward: dx = d(norm)/dx^T dy (+ dres when
+ * non-null), dg [h] fp32 accumulated (+=). */
+int sp_norm_fwd(int32_t dtype, int32_t rms, const void* x, const float* g, void* y, float* mean,
+                float* rstd, int64_t n, int32_t h, float eps, void* stream);
+int sp_norm_bwd(int32_t dtype, int32_t rms, const void* dy, const void* x, const float* g,
+                const float* mean, const float* rstd, const void* dres, void* dx, float* dg,
+                int64_t n, int32_t h, void* stream);
+/* MLP activation: family SP_MODEL_GPT = GeLU(tanh) of u [n, F]; SP_MODEL_LLAMA = SwiGLU of
+ * u [n, 2F] = [gate | up] -> [n, F]. Backward writes du (same shape as u). */
+int sp_act_fwd(int32_t dtype, int32_t family, const void* u, void* out, int64_t n, int32_t F,
+               void* stream);
+int sp_act_bwd(int32_t dtype, int32_t family, const void* u, const void* dout, void* du, int64_t n,
+               int32_t F, void* stream);
 int sp_device_synchronize(int32_t cuda_device);
 int sp_cuda_device_count(int32_t* n);
 

@@ -74,6 +74,29 @@ int sp_attention_bwd(int32_t dtype, int32_t impl, const void* q, const void* kv,
   });
 }
 
+int sp_norm_fwd(int32_t dtype, int32_t rms, const void* x, const float* g, void* y, float* mean, float* rstd,
+                int64_t n, int32_t h, float eps, void* stream) {
+  return cuda_guard([&] {
+    spk::norm_fwd(dt(dtype), rms != 0, x, g, y, mean, rstd, n, h, eps, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int sp_norm_bwd(int32_t dtype, int32_t rms, const void* dy, const void* x, const float* g, const float* mean,
+                const float* rstd, const void* dres, void* dx, float* dg, int64_t n, int32_t h, void* stream) {
+  return cuda_guard([&] {
+    spk::norm_bwd(dt(dtype), rms != 0, dy, x, g, mean, rstd, dres, dx, dg, n, h, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int sp_act_fwd(int32_t dtype, int32_t family, const void* u, void* out, int64_t n, int32_t F, void* stream) {
+  return cuda_guard([&] { spk::act_fwd(dt(dtype), family, u, out, n, F, static_cast<cudaStream_t>(stream)); });
+}
+
+int sp_act_bwd(int32_t dtype, int32_t family, const void* u, const void* dout, void* du, int64_t n, int32_t F,
+               void* stream) {
+  return cuda_guard([&] { spk::act_bwd(dt(dtype), family, u, dout, du, n, F, static_cast<cudaStream_t>(stream)); });
+}
+
 int sp_device_synchronize(int32_t cuda_device) {
   return cuda_guard([&] {
     SPK_CUDA(cudaSetDevice(cuda_device));

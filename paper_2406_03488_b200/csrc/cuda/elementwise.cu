@@ -3,6 +3,7 @@
 // One CTA per row for the row reductions (warp-shuffle + smem reduce), grid
 // sized to a multiple of the SM count for the streaming kernels.
 #include <cmath>
+#include <type_traits>
 
 #include "cuda/common.cuh"
 #include "cuda/ops.h"
@@ -266,6 +267,275 @@ __global__ void adamw_k(float* p, const float* __restrict__ g, float* m, float* 
   }
 }
 
+// ------------------------------------------------------------------ bf16 fast paths
+// Rows of h = 256*NV bf16: one warp per row, each lane owns NV chunks of 8
+// contiguous columns (16-byte loads/stores, fully coalesced), the row stays in
+// registers between the statistics pass and the output pass.
+struct alignas(16) Bf8 {
+  __nv_bfloat162 v[4];
+};
+__device__ __forceinline__ void bf8_to_f(const Bf8& b, float (&f)[8]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 t = __bfloat1622float2(b.v[e]);
+    f[2 * e] = t.x;
+    f[2 * e + 1] = t.y;
+  }
+}
+__device__ __forceinline__ Bf8 f_to_bf8(const float (&f)[8]) {
+  Bf8 b;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) b.v[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+  return b;
+}
+__device__ __forceinline__ void ld_f8(const float* p, float (&f)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+  f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+template <int NV, bool RMS>
+__global__ void __launch_bounds__(256) norm_fwd_vec_k(const __nv_bfloat16* __restrict__ x, const float* __restrict__ g,
+                                                      __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+                                                      float* __restrict__ rstd_out, int64_t n, float eps) {
+  constexpr int H = 256 * NV;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + threadIdx.x / 32;
+  if (row >= n) return;
+  const Bf8* xr = reinterpret_cast<const Bf8*>(x + row * H);
+  Bf8 xv[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) xv[k] = xr[k * 32 + lane];
+  float mean = 0.f;
+  if (!RMS) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float f[8];
+      bf8_to_f(xv[k], f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += f[e];
+    }
+    mean = warp_sum(s) / H;
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    float f[8];
+    bf8_to_f(xv[k], f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ss += (f[e] - mean) * (f[e] - mean);
+  }
+  const float rstd = rsqrtf(warp_sum(ss) / H + eps);
+  Bf8* yr = reinterpret_cast<Bf8*>(y + row * H);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    float f[8], gv[8];
+    bf8_to_f(xv[k], f);
+    ld_f8(g + (k * 32 + lane) * 8, gv);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = (f[e] - mean) * rstd * gv[e];
+    yr[k * 32 + lane] = f_to_bf8(f);
+  }
+  if (lane == 0) {
+    if (!RMS) mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+template <int NV, bool RMS>
+__global__ void __launch_bounds__(256) norm_apply_vec_k(const __nv_bfloat16* __restrict__ x, const float* __restrict__ g,
+                                                        const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                        __nv_bfloat16* __restrict__ y, int64_t n) {
+  constexpr int H = 256 * NV;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + threadIdx.x / 32;
+  if (row >= n) return;
+  const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
+  const Bf8* xr = reinterpret_cast<const Bf8*>(x + row * H);
+  Bf8* yr = reinterpret_cast<Bf8*>(y + row * H);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    float f[8], gv[8];
+    bf8_to_f(xr[k * 32 + lane], f);
+    ld_f8(g + (k * 32 + lane) * 8, gv);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = (f[e] - mu) * rs * gv[e];
+    yr[k * 32 + lane] = f_to_bf8(f);
+  }
+}
+
+// dx = rstd (g*dy - mean(g*dy) - xhat mean(g*dy*xhat)) (+ dres); dg += dy*xhat.
+// Warps stride over rows; each warp accumulates dg for its lane-owned columns in
+// its own shared-memory row (no atomics, no bank conflicts), the block sums its
+// 8 rows and adds them to dg once.
+template <int NV, bool RMS>
+__global__ void __launch_bounds__(256) norm_bwd_vec_k(const __nv_bfloat16* __restrict__ dy,
+                                                      const __nv_bfloat16* __restrict__ x, const float* __restrict__ g,
+                                                      const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                      const __nv_bfloat16* dres, __nv_bfloat16* dx,
+                                                      float* __restrict__ dg, int64_t n) {
+  constexpr int H = 256 * NV;
+  extern __shared__ float4 sdg4[];  // [8 warps][H] fp32
+  float* sdg = reinterpret_cast<float*>(sdg4);
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  float* my = sdg + w * H;
+  for (int c = lane * 4; c < H; c += 128) *reinterpret_cast<float4*>(my + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncwarp();
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + w; row < n; row += static_cast<int64_t>(gridDim.x) * 8) {
+    const Bf8* xr = reinterpret_cast<const Bf8*>(x + row * H);
+    const Bf8* dyr = reinterpret_cast<const Bf8*>(dy + row * H);
+    const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
+    // hd up to 2560 keeps the row in registers between the passes; wider rows
+    // re-read it (L1/L2 hits) instead of spilling.
+    constexpr bool CACHE = NV <= 10;
+    Bf8 xv[CACHE ? NV : 1], dv[CACHE ? NV : 1];
+    if constexpr (CACHE) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        xv[k] = xr[k * 32 + lane];
+        dv[k] = dyr[k * 32 + lane];
+      }
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll(CACHE ? NV : 2)
+    for (int k = 0; k < NV; ++k) {
+      float f[8], d[8], gv[8];
+      bf8_to_f(CACHE ? xv[CACHE ? k : 0] : xr[k * 32 + lane], f);
+      bf8_to_f(CACHE ? dv[CACHE ? k : 0] : dyr[k * 32 + lane], d);
+      ld_f8(g + (k * 32 + lane) * 8, gv);
+      float* acc = my + (k * 32 + lane) * 8;
+      float4 a0 = *reinterpret_cast<float4*>(acc), a1 = *reinterpret_cast<float4*>(acc + 4);
+      float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xh = (f[e] - mu) * rs, dxh = d[e] * gv[e];
+        s1 += dxh;
+        s2 += dxh * xh;
+        av[e] += d[e] * xh;
+      }
+      *reinterpret_cast<float4*>(acc) = make_float4(av[0], av[1], av[2], av[3]);
+      *reinterpret_cast<float4*>(acc + 4) = make_float4(av[4], av[5], av[6], av[7]);
+    }
+    const float m1 = RMS ? 0.f : warp_sum(s1) / H;
+    const float m2 = warp_sum(s2) / H;
+    Bf8* dxr = reinterpret_cast<Bf8*>(dx + row * H);
+    const Bf8* drr = dres ? reinterpret_cast<const Bf8*>(dres + row * H) : nullptr;
+#pragma unroll(CACHE ? NV : 2)
+    for (int k = 0; k < NV; ++k) {
+      float f[8], d[8], gv[8], r[8];
+      bf8_to_f(CACHE ? xv[CACHE ? k : 0] : xr[k * 32 + lane], f);
+      bf8_to_f(CACHE ? dv[CACHE ? k : 0] : dyr[k * 32 + lane], d);
+      ld_f8(g + (k * 32 + lane) * 8, gv);
+      if (drr) bf8_to_f(drr[k * 32 + lane], r);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xh = (f[e] - mu) * rs;
+        f[e] = rs * (d[e] * gv[e] - m1 - xh * m2) + (drr ? r[e] : 0.f);
+      }
+      dxr[k * 32 + lane] = f_to_bf8(f);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < H; c += 256) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += sdg[k * H + c];
+    atomicAdd(&dg[c], s);
+  }
+}
+
+__device__ __forceinline__ float gelu_f(float u) { return gelu_tanh(u); }
+
+// GeLU (family 0) / SwiGLU (family 1) over 8-element vectors.
+__global__ void act_fwd_vec_k(int family, const __nv_bfloat16* __restrict__ u, __nv_bfloat16* __restrict__ g,
+                              int64_t n, int F) {
+  const int64_t chunks = n * F / 8, per_row = F / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunks; i += (int64_t)gridDim.x * blockDim.x) {
+    float a[8];
+    if (family == 0) {
+      bf8_to_f(reinterpret_cast<const Bf8*>(u)[i], a);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] = gelu_tanh(a[e]);
+    } else {
+      const int64_t r = i / per_row, c = i % per_row;
+      float b[8];
+      bf8_to_f(reinterpret_cast<const Bf8*>(u)[r * 2 * per_row + c], a);
+      bf8_to_f(reinterpret_cast<const Bf8*>(u)[r * 2 * per_row + per_row + c], b);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] = a[e] * sigmoidf_(a[e]) * b[e];
+    }
+    reinterpret_cast<Bf8*>(g)[i] = f_to_bf8(a);
+  }
+}
+
+__global__ void act_bwd_vec_k(int family, const __nv_bfloat16* __restrict__ u, const __nv_bfloat16* dg,
+                              __nv_bfloat16* du, int64_t n, int F) {
+  const int64_t chunks = n * F / 8, per_row = F / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunks; i += (int64_t)gridDim.x * blockDim.x) {
+    float d[8];
+    bf8_to_f(reinterpret_cast<const Bf8*>(dg)[i], d);
+    if (family == 0) {
+      float a[8];
+      bf8_to_f(reinterpret_cast<const Bf8*>(u)[i], a);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] = d[e] * gelu_tanh_grad(a[e]);
+      reinterpret_cast<Bf8*>(du)[i] = f_to_bf8(a);
+    } else {
+      const int64_t r = i / per_row, c = i % per_row;
+      float a[8], b[8];
+      bf8_to_f(reinterpret_cast<const Bf8*>(u)[r * 2 * per_row + c], a);
+      bf8_to_f(reinterpret_cast<const Bf8*>(u)[r * 2 * per_row + per_row + c], b);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float s = sigmoidf_(a[e]);
+        const float da = d[e] * b[e] * s * (1.f + a[e] * (1.f - s)), db = d[e] * a[e] * s;
+        a[e] = da;
+        b[e] = db;
+      }
+      reinterpret_cast<Bf8*>(du)[r * 2 * per_row + c] = f_to_bf8(a);
+      reinterpret_cast<Bf8*>(du)[r * 2 * per_row + per_row + c] = f_to_bf8(b);
+    }
+  }
+}
+
+// [dq | dk | dv] rows for the QKV dgrad / wgrad GEMMs: dq bf16 [n, h], dK/dV
+// fp32 rows of the accumulator [n, 2h] -> bf16 [n, 3h]; 8 columns per thread.
+__global__ void assemble_dqkv_vec_k(const __nv_bfloat16* __restrict__ dq, const float* __restrict__ dkv,
+                                    __nv_bfloat16* __restrict__ out, int64_t n, int h) {
+  const int64_t per_row = 3 * h / 8, chunks = n * per_row;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunks; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / per_row;
+    const int c = static_cast<int>(i % per_row) * 8;
+    if (c < h) {
+      reinterpret_cast<Bf8*>(out)[i] = reinterpret_cast<const Bf8*>(dq + r * h + c)[0];
+    } else {
+      float f[8];
+      const float* src = dkv + r * 2 * h + (c - h);
+      const float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4);
+      f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+      reinterpret_cast<Bf8*>(out)[i] = f_to_bf8(f);
+    }
+  }
+}
+
+// NV dispatch for the row kernels (h = 256 * NV); false = no fast path.
+template <typename F>
+bool dispatch_nv(int h, F&& f) {
+  if (h % 256) return false;
+  switch (h / 256) {
+    case 1: f(std::integral_constant<int, 1>{}); return true;
+    case 2: f(std::integral_constant<int, 2>{}); return true;
+    case 4: f(std::integral_constant<int, 4>{}); return true;
+    case 8: f(std::integral_constant<int, 8>{}); return true;
+    case 10: f(std::integral_constant<int, 10>{}); return true;
+    case 12: f(std::integral_constant<int, 12>{}); return true;
+    case 16: f(std::integral_constant<int, 16>{}); return true;
+    case 20: f(std::integral_constant<int, 20>{}); return true;
+    default: return false;
+  }
+}
+
 }  // namespace
 
 #define SPK_DISPATCH(t, ...)                 \
@@ -292,6 +562,19 @@ void embed_bwd(DType t, const int32_t* tok, const void* dx, float* dE, float* dp
 void norm_fwd(DType t, bool rms, const void* x, const float* g, void* y, float* mean, float* rstd, int64_t n, int h,
               float eps, cudaStream_t s) {
   if (n == 0) return;
+  if (t == DType::kBF16 && dispatch_nv(h, [&](auto nv) {
+        constexpr int NV = decltype(nv)::value;
+        const unsigned grid = static_cast<unsigned>((n + 7) / 8);
+        const auto* xb = static_cast<const __nv_bfloat16*>(x);
+        auto* yb = static_cast<__nv_bfloat16*>(y);
+        if (rms)
+          norm_fwd_vec_k<NV, true><<<grid, 256, 0, s>>>(xb, g, yb, mean, rstd, n, eps);
+        else
+          norm_fwd_vec_k<NV, false><<<grid, 256, 0, s>>>(xb, g, yb, mean, rstd, n, eps);
+      })) {
+    SPK_LAUNCH_CHECK();
+    return;
+  }
   SPK_DISPATCH(t, {
     if (rms)
       norm_fwd_k<T, true><<<n, kRowThreads, 0, s>>>((const T*)x, g, (T*)y, mean, rstd, h, eps);
@@ -303,6 +586,20 @@ void norm_fwd(DType t, bool rms, const void* x, const float* g, void* y, float* 
 
 void norm_apply(DType t, bool rms, const void* x, const float* g, const float* mean, const float* rstd, void* y,
                 int64_t n, int h, cudaStream_t s) {
+  if (n == 0) return;
+  if (t == DType::kBF16 && dispatch_nv(h, [&](auto nv) {
+        constexpr int NV = decltype(nv)::value;
+        const unsigned grid = static_cast<unsigned>((n + 7) / 8);
+        const auto* xb = static_cast<const __nv_bfloat16*>(x);
+        auto* yb = static_cast<__nv_bfloat16*>(y);
+        if (rms)
+          norm_apply_vec_k<NV, true><<<grid, 256, 0, s>>>(xb, g, mean, rstd, yb, n);
+        else
+          norm_apply_vec_k<NV, false><<<grid, 256, 0, s>>>(xb, g, mean, rstd, yb, n);
+      })) {
+    SPK_LAUNCH_CHECK();
+    return;
+  }
   SPK_DISPATCH(t, {
     if (rms)
       norm_apply_k<T, true><<<stream_grid(n * h, 256), 256, 0, s>>>((const T*)x, g, mean, rstd, (T*)y, n, h);
@@ -315,6 +612,24 @@ void norm_apply(DType t, bool rms, const void* x, const float* g, const float* m
 void norm_bwd(DType t, bool rms, const void* dy, const void* x, const float* g, const float* mean, const float* rstd,
               const void* dres, void* dx, float* dg, int64_t n, int h, cudaStream_t s) {
   if (n == 0) return;
+  if (t == DType::kBF16 && dispatch_nv(h, [&](auto nv) {
+        constexpr int NV = decltype(nv)::value;
+        const size_t sm = sizeof(float) * 8 * 256 * NV;
+        const int64_t blocks = (n + 7) / 8;
+        const unsigned grid = static_cast<unsigned>(blocks < num_sms() ? blocks : num_sms());
+        auto launch = [&](auto kern) {
+          SPK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+          kern<<<grid, 256, sm, s>>>(static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), g, mean,
+                                     rstd, static_cast<const __nv_bfloat16*>(dres), static_cast<__nv_bfloat16*>(dx), dg, n);
+        };
+        if (rms)
+          launch(norm_bwd_vec_k<NV, true>);
+        else
+          launch(norm_bwd_vec_k<NV, false>);
+      })) {
+    SPK_LAUNCH_CHECK();
+    return;
+  }
   const int grid = static_cast<int>(n < 2 * num_sms() ? n : 2 * num_sms());
   const size_t smem = sizeof(float) * h;
   SPK_DISPATCH(t, {
@@ -332,11 +647,24 @@ void norm_bwd(DType t, bool rms, const void* dy, const void* x, const float* g, 
 }
 
 void act_fwd(DType t, int family, const void* u, void* g, int64_t n, int F, cudaStream_t s) {
+  if (t == DType::kBF16 && F % 8 == 0) {
+    act_fwd_vec_k<<<stream_grid(n * F / 8, 256), 256, 0, s>>>(family, static_cast<const __nv_bfloat16*>(u),
+                                                               static_cast<__nv_bfloat16*>(g), n, F);
+    SPK_LAUNCH_CHECK();
+    return;
+  }
   SPK_DISPATCH(t, act_fwd_k<T><<<stream_grid(n * F, 256), 256, 0, s>>>(family, (const T*)u, (T*)g, n, F));
   SPK_LAUNCH_CHECK();
 }
 
 void act_bwd(DType t, int family, const void* u, const void* dg, void* du, int64_t n, int F, cudaStream_t s) {
+  if (t == DType::kBF16 && F % 8 == 0) {
+    act_bwd_vec_k<<<stream_grid(n * F / 8, 256), 256, 0, s>>>(family, static_cast<const __nv_bfloat16*>(u),
+                                                               static_cast<const __nv_bfloat16*>(dg),
+                                                               static_cast<__nv_bfloat16*>(du), n, F);
+    SPK_LAUNCH_CHECK();
+    return;
+  }
   SPK_DISPATCH(t, act_bwd_k<T><<<stream_grid(n * F, 256), 256, 0, s>>>(family, (const T*)u, (const T*)dg, (T*)du, n, F));
   SPK_LAUNCH_CHECK();
 }
@@ -348,6 +676,12 @@ void rope(DType t, void* x, int64_t ld, int64_t n, int H, int hd, int64_t pos0, 
 }
 
 void assemble_dqkv(DType t, const void* dq, const float* dkv, void* dqkv, int64_t n, int h, cudaStream_t s) {
+  if (t == DType::kBF16 && h % 8 == 0) {
+    assemble_dqkv_vec_k<<<stream_grid(n * 3 * h / 8, 256), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dq), dkv,
+                                                                          static_cast<__nv_bfloat16*>(dqkv), n, h);
+    SPK_LAUNCH_CHECK();
+    return;
+  }
   SPK_DISPATCH(t, assemble_dqkv_k<T><<<stream_grid(n * 3 * h, 256), 256, 0, s>>>((const T*)dq, dkv, (T*)dqkv, n, h));
   SPK_LAUNCH_CHECK();
 }

@@ -126,3 +126,63 @@ def test_attention_fwd_bwd(gpu, dtype, impl, n, q_off, H, hd):
     assert _rel(dq.float(), dq_ref) < tolb
     assert _rel(dkv[:, :h] - base[:, :h], dk) < tolb
     assert _rel(dkv[:, h:] - base[:, h:], dv) < tolb
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+@pytest.mark.parametrize("rms", [0, 1])
+@pytest.mark.parametrize("n,h", [(37, 256), (301, 2560), (64, 4096), (9, 5120), (50, 384)])
+def test_norm_fwd_bwd(gpu, rms, n, h):
+    """Vectorised bf16 row norms (h = 256*NV fast path; h = 384 generic) vs torch fp32."""
+    g = torch.Generator(device="cuda").manual_seed(n * 7 + h)
+    x = (torch.randn(n, h, device="cuda", generator=g) * 2 + 0.5).to(torch.bfloat16)
+    gain = torch.rand(h, device="cuda", generator=g) + 0.5
+    dy = torch.randn(n, h, device="cuda", generator=g).to(torch.bfloat16)
+    dres = torch.randn(n, h, device="cuda", generator=g).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    mean = torch.zeros(n, device="cuda")
+    rstd = torch.zeros(n, device="cuda")
+    lib = _capi.lib()
+    _capi.check(lib.sp_norm_fwd(BF16, rms, _p(x), _p(gain), _p(y), _p(mean), _p(rstd), n, h, 1e-5, None))
+    xf = x.float().requires_grad_(True)
+    gf = gain.clone().requires_grad_(True)
+    if rms:
+        ref = xf * torch.rsqrt((xf * xf).mean(-1, keepdim=True) + 1e-5) * gf
+    else:
+        ref = torch.nn.functional.layer_norm(xf, (h,), weight=gf, eps=1e-5)
+    assert _rel(y.float(), ref.detach()) < 1e-2
+    ref.backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.zeros(h, device="cuda")
+    _capi.check(lib.sp_norm_bwd(BF16, rms, _p(dy), _p(x), _p(gain), _p(mean), _p(rstd), _p(dres), _p(dx), _p(dg), n, h,
+                                None))
+    torch.cuda.synchronize()
+    assert _rel(dx.float(), xf.grad + dres.float()) < 1e-2
+    assert _rel(dg, gf.grad) < 1e-3
+
+
+@pytest.mark.parametrize("family", [0, 1])
+@pytest.mark.parametrize("n,F", [(33, 1024), (129, 10240), (17, 11008)])
+def test_activation_fwd_bwd(gpu, family, n, F):
+    """GeLU(tanh) / SwiGLU bf16 kernels (8-wide vector path) vs torch fp32."""
+    g = torch.Generator(device="cuda").manual_seed(n + F + family)
+    width = F if family == 0 else 2 * F
+    u = torch.randn(n, width, device="cuda", generator=g).to(torch.bfloat16)
+    d = torch.randn(n, F, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.empty(n, F, device="cuda", dtype=torch.bfloat16)
+    du = torch.empty_like(u)
+    lib = _capi.lib()
+    _capi.check(lib.sp_act_fwd(BF16, family, _p(u), _p(out), n, F, None))
+    uf = u.float().requires_grad_(True)
+    if family == 0:
+        ref = torch.nn.functional.gelu(uf, approximate="tanh")
+    else:
+        a, b = uf[:, :F], uf[:, F:]
+        ref = torch.nn.functional.silu(a) * b
+    assert _rel(out.float(), ref.detach()) < 1e-2
+    ref.backward(d.float())
+    _capi.check(lib.sp_act_bwd(BF16, family, _p(u), _p(d), _p(du), n, F, None))
+    torch.cuda.synchronize()
+    assert _rel(du.float(), uf.grad) < 1e-2
