@@ -37,11 +37,22 @@ WORKLOAD = "GPT-2.7B seq 32K, 4 sub-sequences (cwp), Seq1F1B, pipeline depth = G
 
 
 def peaks():
+    """(burst, sustained) bf16 TFLOP/s and HBM GB/s: MEASURED_PEAKS.json when the driver wrote it,
+    else the fallback figures of the B200 profiling recipe."""
     try:
         d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
         return d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), d["hbm_gbs"], "measured"
     except Exception:
         return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def traffic_of(kernel):
+    """DRAM bytes per launch of the dominant kernel class from the committed ncu capture."""
+    try:
+        d = json.loads((ROOT / "profiles" / "r1_traffic.json").read_text())[kernel]
+        return d["dram_bytes_per_launch"], d["launch"]
+    except Exception:
+        return None, None
 
 
 def model_and_cfg(n_gpus: int, seq: int, micro: int, k: int, dtype_bf16=True):
@@ -331,13 +342,17 @@ def main():
                        "schedule": args.kind, "parallelism": f"pp{args.gpus}",
                        "l2": "inputs larger than L2 (weights+activations >> 126 MB)"},
             "tflops_per_gpu": fl / (step_ms / 1e3) / 1e12 / args.gpus,
-            "model_flops_frac_of_peak": fl / (step_ms / 1e3) / 1e12 / args.gpus / burst,
+            "model_flops_frac_of_peak": fl / (step_ms / 1e3) / 1e12 / args.gpus / sustained,
             "bubble_ratio": bubble, "modeled": modeled,
             "peak_activation_gb_per_stage": peak_act,
             "batch_level_1f1b": mem_1f1b,
-            "roofline": {"bound": "tensor", "kernel": names[dom], "achieved": achieved, "peak": burst,
-                         "peak_kind": f"bf16 burst ({src})", "unit": "TFLOP/s",
-                         "frac": (achieved / burst) if achieved else None, "traffic": None,
+            # Kernels timed inside a seconds-long step run under the power cap: the
+            # denominator is the sustained bf16 figure (burst reported beside it).
+            "roofline": {"bound": "tensor", "kernel": names[dom], "achieved": achieved, "peak": sustained,
+                         "peak_kind": f"bf16 sustained ({src})", "peak_burst": burst, "unit": "TFLOP/s",
+                         "frac": (achieved / sustained) if achieved else None,
+                         "frac_of_burst": (achieved / burst) if achieved else None,
+                         "traffic": traffic_of(names[dom])[0], "traffic_launch": traffic_of(names[dom])[1],
                          "classes": {names[c]: {"ms": cls_ms[c], "tflops": (cls_fl[c] / cls_ms[c] / 1e9)
                                                 if cls_ms[c] else None, "launches": cls_n[c]} for c in range(3)}},
             "cpu_baseline": cpu,
