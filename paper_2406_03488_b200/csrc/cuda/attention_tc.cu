@@ -125,6 +125,7 @@ __device__ __forceinline__ void load_tile(uint8_t* dst, const Maps& t, uint64_t*
 struct __align__(64) AttnParams {
   Maps tq;   // q [n, h], 128-row boxes
   Maps tkv;  // kv [kv_len, 2h], 128-row boxes
+  const __nv_bfloat16* q;  // raw rows (copied into TMEM as the S-MMA A operand, hd <= 80)
   __nv_bfloat16* o;
   float* lse;
   int64_t n, q_off, kv_len;
@@ -231,11 +232,58 @@ __host__ __device__ constexpr bool poly_group(int g) { return SPK_POLY_FWD > 0 &
 __host__ __device__ constexpr bool bwd_poly_group(int g) { return SPK_POLY_BWD > 0 && poly_pick(g, SPK_POLY_BWD); }
 __host__ __device__ constexpr bool dq_poly_group(int g) { return SPK_POLY_DQ > 0 && poly_pick(g, SPK_POLY_DQ); }
 
+// Copy this lane's [HD] bf16 row (`src`, or zeros when !valid) into TMEM as an
+// MMA A operand: column c of the lane holds elements (2c, 2c+1).
+template <int HD>
+__device__ __forceinline__ void row_to_tmem(uint32_t taddr, const __nv_bfloat16* src, bool valid) {
+  uint32_t v[HD / 2];
+#pragma unroll
+  for (int c = 0; c < HD / 8; ++c) {
+    const uint4 u = valid ? __ldg(reinterpret_cast<const uint4*>(src) + c) : make_uint4(0, 0, 0, 0);
+    v[4 * c] = u.x;
+    v[4 * c + 1] = u.y;
+    v[4 * c + 2] = u.z;
+    v[4 * c + 3] = u.w;
+  }
+#pragma unroll
+  for (int c = 0; c < HD / 16; ++c) tc::tmem_st8(taddr + 8 * c, v + 8 * c);
+}
+
+// Same for half of the row: elements [0, HD/2) of `src` -> HD/4 columns at taddr.
+template <int HD>
+__device__ __forceinline__ void row_part_to_tmem(uint32_t taddr, const __nv_bfloat16* src, bool valid) {
+  constexpr int NC = HD / 4;  // 32-bit columns (bf16 pairs): 20 (hd 80) / 16 (hd 64) / 32 (hd 128)
+  uint32_t v[NC];
+#pragma unroll
+  for (int c = 0; c < NC / 4; ++c) {
+    const uint4 u = valid ? __ldg(reinterpret_cast<const uint4*>(src) + c) : make_uint4(0, 0, 0, 0);
+    v[4 * c] = u.x;
+    v[4 * c + 1] = u.y;
+    v[4 * c + 2] = u.z;
+    v[4 * c + 3] = u.w;
+  }
+#pragma unroll
+  for (int c = 0; c + 8 <= NC; c += 8) tc::tmem_st8(taddr + c, v + c);
+  if constexpr (NC % 8 == 4) tc::tmem_st4(taddr + NC - 4, v + NC - 4);
+}
+
+// Forward CTA = two 128-query tiles (A, B) of one head, ping-ponged so that one
+// tile's softmax overlaps the other tile's MMAs. TMEM (512 columns):
+//   S_A [0,128) | S_B [128,256) | O_A, Q_A (hd <= 80: Q as TS-MMA A operand) | O_B, Q_B
+// hd 128 keeps Q in shared memory (SS form): S_A | S_B | O_A [256,384) | O_B [384,512).
+template <int HD>
+struct FwdCfg {
+  static constexpr bool QT = HD <= 80;
+  __host__ __device__ static constexpr uint32_t t_o(int t) { return t ? 384 : 256; }
+  __host__ __device__ static constexpr uint32_t t_q(int t) { return t_o(t) + HD; }
+  static_assert(!QT || 384 + HD + HD / 2 <= 512, "fwd TMEM budget");
+};
+
 template <int HD>
 constexpr size_t fwd_smem_n(int st) {
-  return Lay<HD>::bytes(128) * (1 + 2 * st) + (10 + 4 * st) * 8 + 8 + 1024;
+  return (FwdCfg<HD>::QT ? 0 : 2 * Lay<HD>::bytes(128)) + 2 * st * Lay<HD>::bytes(128) + (16 + 4 * st) * 8 + 8 + 1024;
 }
-// Ring depths: as many stages as the opt-in SMEM (227 KB) holds, capped at 4 / 6 / 8.
+// Ring depths: as many K / V stages as the opt-in SMEM (227 KB) holds, capped at 6.
 template <int HD>
 constexpr int fwd_stages() {
   int st = 6;
@@ -250,20 +298,21 @@ constexpr size_t fwd_smem() {
 // ============================================================================ forward
 
 template <int HD>
-__global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ AttnParams p) {
+__global__ void __launch_bounds__(384, 1) attn_fwd_tc_k(const __grid_constant__ AttnParams p) {
+  using C = FwdCfg<HD>;
   constexpr int KVS = fwd_stages<HD>();
   constexpr int TB = Lay<HD>::bytes(128);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;
-  uint8_t* sK = sQ + TB;           // [KVS]
-  uint8_t* sV = sK + KVS * TB;     // [KVS]
+  uint8_t* sQ = sm;                          // [2] (hd 128 only)
+  uint8_t* sK = sQ + (C::QT ? 0 : 2 * TB);   // [KVS]
+  uint8_t* sV = sK + KVS * TB;               // [KVS]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + KVS * TB);
-  uint64_t* q_full = bars;
-  uint64_t* s_full = bars + 1;   // [2]
-  uint64_t* p_full = bars + 5;   // [2]
-  uint64_t* p_empty = bars + 7;  // [2]
-  uint64_t* k_full = bars + 10;          // [KVS]
+  uint64_t* q_ready = bars;      // Q of both tiles resident (TMEM copy or TMA)
+  uint64_t* s_full = bars + 1;   // [2 tiles]
+  uint64_t* p_full = bars + 3;   // [2 tiles]  P packed into the tile's S buffer
+  uint64_t* pv_done = bars + 5;  // [2 tiles]  O += P V completed
+  uint64_t* k_full = bars + 16;          // [KVS]
   uint64_t* k_empty = k_full + KVS;      // [KVS]
   uint64_t* v_full = k_empty + KVS;      // [KVS]
   uint64_t* v_empty = v_full + KVS;      // [KVS]
@@ -271,19 +320,31 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int num_qb = static_cast<int>((p.n + BQ - 1) / BQ);
-  const int qb = num_qb - 1 - static_cast<int>(blockIdx.x);  // heaviest blocks first
+  const int npair = (num_qb + 1) / 2;
+  const int pair = npair - 1 - static_cast<int>(blockIdx.x);  // heaviest pairs first
   const int head = blockIdx.y;
-  const int64_t q0 = static_cast<int64_t>(qb) * BQ;
-  const int64_t q_hi = (q0 + BQ < p.n ? q0 + BQ : p.n);
-  const int64_t kend = (p.q_off + q_hi < p.kv_len) ? p.q_off + q_hi : p.kv_len;
-  const int nblk = static_cast<int>((kend + BKV - 1) / BKV);
+  int nblk_t[2];
+  int64_t q0_t[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int qb = 2 * pair + t;
+    q0_t[t] = static_cast<int64_t>(qb) * BQ;
+    if (qb >= num_qb) {
+      nblk_t[t] = 0;
+      continue;
+    }
+    const int64_t q_hi = (q0_t[t] + BQ < p.n ? q0_t[t] + BQ : p.n);
+    const int64_t kend = (p.q_off + q_hi < p.kv_len) ? p.q_off + q_hi : p.kv_len;
+    nblk_t[t] = static_cast<int>((kend + BKV - 1) / BKV);
+  }
+  const int nblk = nblk_t[0] > nblk_t[1] ? nblk_t[0] : nblk_t[1];
 
   if (threadIdx.x == 0) {
-    tc::mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&p_full[i], 4);  // softmax warps
-      tc::mbar_init(&p_empty[i], 1);
+    tc::mbar_init(q_ready, C::QT ? 8 : 1);  // softmax warps (TMEM copy) or the TMA
+    for (int t = 0; t < 2; ++t) {
+      tc::mbar_init(&s_full[t], 1);
+      tc::mbar_init(&p_full[t], 4);  // the tile's softmax warps
+      tc::mbar_init(&pv_done[t], 1);
     }
     for (int i = 0; i < KVS; ++i) {
       tc::mbar_init(&k_full[i], 1);
@@ -298,17 +359,18 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform (keeps MMA operands in uniform registers)
-  // TMEM: S0 [0,128) S1 [128,256) O [256, 256+hd). P_j (bf16) overwrites the
-  // first 64 columns of its S buffer and feeds the PV MMA straight from TMEM.
 
   if (warp == 0) {
     if (lane == 0) {
-      tc::tma_prefetch(&p.tq.m0);
       tc::tma_prefetch(&p.tkv.m0);
-      tc::mbar_expect_tx(q_full, TB);
-      load_tile<HD>(sQ, p.tq, q_full, head * HD, static_cast<int>(q0), 128, 0);
-      // K runs one block ahead of V: K_{j+1} (freed after S_{j+1-KVS}) is
-      // requested before V_j (freed after PV_{j-KVS}), so PV never starves S.
+      if constexpr (!C::QT) {
+        tc::tma_prefetch(&p.tq.m0);
+        tc::mbar_expect_tx(q_ready, (nblk_t[1] > 0 ? 2 : 1) * TB);
+        for (int t = 0; t < 2; ++t)
+          if (nblk_t[t] > 0) load_tile<HD>(sQ + t * TB, p.tq, q_ready, head * HD, static_cast<int>(q0_t[t]), 128, 0);
+      }
+      // K runs one block ahead of V: K_{j+1} (freed after S(j+1-KVS)) is
+      // requested before V_j (freed after PV(j-KVS)), so PV never starves S.
       auto load_k = [&](int j) {
         const int st = j % KVS;
         tc::mbar_wait(&k_empty[st], ((j / KVS) & 1) ^ 1);
@@ -325,63 +387,79 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
       }
     }
   } else if (warp == 1) {
-    {  // whole warp, converged: tc::*_w helpers elect the issuing lane
-      constexpr uint32_t idesc_s = tc::idesc_bf16(128, BKV, false, false);
-      tc::mbar_wait_w(q_full, 0);
-      const uint32_t q_base = tc::smem_u32(sQ);
-      // Static issue order with blocking waits (an mbarrier try_wait wakes ~60
-      // cycles after the arrive; polling with test_wait costs ~150 per probe):
-      // S_0, S_1, then per block j: PV_j once P_j is in TMEM, then S_{j+2} into
-      // the buffer PV_j just read (MMAs execute in issue order).
-      auto issue_s = [&](int j) {
-        const int b = j & 1, st = j % KVS;
-        tc::mbar_wait_w(&k_full[st], (j / KVS) & 1);
-        tc::tc_fence_after();
-        const uint32_t k_base = tc::smem_u32(sK + st * TB);
+    // S-issuing warp (converged; tc::*_w elect the issuing lane): S_t(j) = Q_t K_j^T
+    // once K_j landed and PV_t(j-1) (which read P_t(j-1) from the same buffer)
+    // completed.
+    constexpr uint32_t idesc_s = tc::idesc_bf16(128, BKV, false, false);
+    tc::mbar_wait_w(q_ready, 0);
+    tc::tc_fence_after();
+    for (int j = 0; j < nblk; ++j) {
+      const int st = j % KVS;
+      tc::mbar_wait_w(&k_full[st], (j / KVS) & 1);
+      const uint32_t k_base = tc::smem_u32(sK + st * TB);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          tc::mma_bf16_ss_w(tmem + b * 128, kdesc<HD>(q_base, 128, kk), kdesc<HD>(k_base, 128, kk), idesc_s, kk > 0);
-        tc::mma_commit_w(&s_full[b]);
-        tc::mma_commit_w(&k_empty[st]);
-      };
-      for (int j = 0; j < 2 && j < nblk; ++j) issue_s(j);
-      for (int j = 0; j < nblk; ++j) {
-        const int b = j & 1, st = j % KVS;
-        tc::mbar_wait_w(&p_full[b], (j >> 1) & 1);
-        tc::mbar_wait_w(&v_full[st], (j / KVS) & 1);
+      for (int t = 0; t < 2; ++t) {
+        if (j >= nblk_t[t]) continue;
+        if (j > 0) tc::mbar_wait_w(&pv_done[t], (j - 1) & 1);
         tc::tc_fence_after();
-        const uint32_t v_base = tc::smem_u32(sV + st * TB);
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)  // O accumulates in TMEM; A = P_j from TMEM
-          mma_nhd_ts<HD>(tmem + 256, tmem + b * 128 + kk * 8, v_base, 128, kk, j > 0 || kk > 0);
-        tc::mma_commit_w(&p_empty[b]);  // also marks PV_j (and every earlier MMA) complete
-        tc::mma_commit_w(&v_empty[st]);
-        if (j + 2 < nblk) issue_s(j + 2);
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          if constexpr (C::QT)
+            tc::mma_bf16_ts_w(tmem + t * 128, tmem + C::t_q(t) + 8 * kk, kdesc<HD>(k_base, 128, kk), idesc_s, kk > 0);
+          else
+            tc::mma_bf16_ss_w(tmem + t * 128, kdesc<HD>(tc::smem_u32(sQ + t * TB), 128, kk), kdesc<HD>(k_base, 128, kk),
+                              idesc_s, kk > 0);
+        }
+        tc::mma_commit_w(&s_full[t]);
       }
+      tc::mma_commit_w(&k_empty[st]);
+    }
+  } else if (warp == 2) {
+    // PV-issuing warp: O_t += P_t(j) V_j (A = P from TMEM) once P_t(j) is packed.
+    for (int j = 0; j < nblk; ++j) {
+      const int st = j % KVS;
+      tc::mbar_wait_w(&v_full[st], (j / KVS) & 1);
+      const uint32_t v_base = tc::smem_u32(sV + st * TB);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (j >= nblk_t[t]) continue;
+        tc::mbar_wait_w(&p_full[t], j & 1);
+        tc::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_nhd_ts<HD>(tmem + C::t_o(t), tmem + t * 128 + kk * 8, v_base, 128, kk, j > 0 || kk > 0);
+        tc::mma_commit_w(&pv_done[t]);
+      }
+      tc::mma_commit_w(&v_empty[st]);
     }
   } else if (warp >= 4) {
-    // Softmax: S row in registers (one pass), P -> TMEM, O stays in TMEM. The
-    // running max used for exponentiation only moves when a block raises it by
-    // more than 2^8 (log2 domain); then the O row in TMEM is rescaled once
-    // PV_{j-1} has landed. Otherwise the softmax never waits for the PV MMAs.
-    const int quarter = warp & 3;
+    // Softmax of tile t = (warp-4)/4, one query row per thread: S row in
+    // registers (one pass), P -> TMEM, O stays in TMEM. The running max used for
+    // exponentiation only moves when a block raises it by more than 2^8 (log2
+    // domain); then the O row in TMEM is rescaled once PV_t(j-1) has landed.
+    const int t = (warp - 4) >> 2, quarter = warp & 3;
     const int r = quarter * 32 + lane;
-    const int64_t row = q0 + r;
-    const bool valid = row < p.n;
+    const int64_t row = q0_t[t] + r;
+    const bool valid = nblk_t[t] > 0 && row < p.n;
     const int64_t qpos = p.q_off + row;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t obase = tmem + lane_base + 256;
+    const uint32_t obase = tmem + lane_base + C::t_o(t);
+    const int nb = nblk_t[t];
+    if constexpr (C::QT) {
+      row_to_tmem<HD>(tmem + lane_base + C::t_q(t), p.q + (valid ? row : 0) * p.h + head * HD, valid);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      warp_arrive(q_ready);
+    }
     constexpr float kRescale = 8.f;
     float m = -INFINITY, l = 0.f;
 
-    for (int j = 0; j < nblk; ++j) {
-      const int b = j & 1;
-      const uint32_t ph = (j >> 1) & 1;
+    for (int j = 0; j < nb; ++j) {
       const int64_t lim64 = (valid ? (qpos < p.kv_len - 1 ? qpos : p.kv_len - 1) : -1) - static_cast<int64_t>(j) * BKV;
       const int lim = lim64 > 1000000 ? 1000000 : static_cast<int>(lim64);  // columns <= lim are visible
-      tc::mbar_wait(&s_full[b], ph);
+      tc::mbar_wait(&s_full[t], j & 1);
       tc::tc_fence_after();
-      const uint32_t sbase = tmem + lane_base + b * 128;
+      const uint32_t sbase = tmem + lane_base + t * 128;
       uint32_t sv[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tc::tmem_ld32(sbase + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
@@ -410,11 +488,9 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
       if (__any_sync(0xffffffffu, need)) {
         const float m_new = need ? fmaxf(m, mx) : m;
         const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
-        if (j > 0) {  // rescale the O row accumulated so far (PV_{j-1} must have landed)
-          // PV_{j-1} landed <=> phase (j-1)>>1 of p_empty[(j-1)&1] completed. The
-          // softmax already waited for that buffer's previous phase, so the
-          // parity wait cannot alias an older phase.
-          tc::mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        if (j > 0) {  // rescale the O row accumulated so far (PV_t(j-1) must have landed)
+          // pv_done[t] cannot be past phase j-1 here: PV_t(j) needs this P_t(j).
+          tc::mbar_wait(&pv_done[t], (j - 1) & 1);
           tc::tc_fence_after();
 #pragma unroll
           for (int c = 0; c < HD / 16; ++c) {
@@ -451,30 +527,32 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_k(const __grid_constant__ 
       l += (rs_a.x + rs_a.y) + (rs_b.x + rs_b.y);
       tc::tmem_st_wait();
       tc::tc_fence_before();
-      warp_arrive(&p_full[b]);
+      warp_arrive(&p_full[t]);
     }
-    if (nblk > 0) tc::mbar_wait(&p_empty[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);  // last PV landed
-    tc::tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* orow = p.o + (valid ? row : 0) * p.h + head * HD;
+    if (nb > 0) {
+      tc::mbar_wait(&pv_done[t], (nb - 1) & 1);  // last PV_t landed
+      tc::tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      __nv_bfloat16* orow = p.o + (valid ? row : 0) * p.h + head * HD;
 #pragma unroll
-    for (int c = 0; c < HD / 16; ++c) {
-      uint32_t v[16];
-      tmem_ld16(obase + c * 16, v);  // warp-collective
-      tc::tmem_ld_wait();
-      if (!valid) continue;
-      uint4 u0 = make_uint4(pack_bf16(__uint_as_float(v[0]) * inv, __uint_as_float(v[1]) * inv),
-                            pack_bf16(__uint_as_float(v[2]) * inv, __uint_as_float(v[3]) * inv),
-                            pack_bf16(__uint_as_float(v[4]) * inv, __uint_as_float(v[5]) * inv),
-                            pack_bf16(__uint_as_float(v[6]) * inv, __uint_as_float(v[7]) * inv));
-      uint4 u1 = make_uint4(pack_bf16(__uint_as_float(v[8]) * inv, __uint_as_float(v[9]) * inv),
-                            pack_bf16(__uint_as_float(v[10]) * inv, __uint_as_float(v[11]) * inv),
-                            pack_bf16(__uint_as_float(v[12]) * inv, __uint_as_float(v[13]) * inv),
-                            pack_bf16(__uint_as_float(v[14]) * inv, __uint_as_float(v[15]) * inv));
-      *reinterpret_cast<uint4*>(orow + c * 16) = u0;
-      *reinterpret_cast<uint4*>(orow + c * 16 + 8) = u1;
+      for (int c = 0; c < HD / 16; ++c) {
+        uint32_t v[16];
+        tmem_ld16(obase + c * 16, v);  // warp-collective
+        tc::tmem_ld_wait();
+        if (!valid) continue;
+        uint4 u0 = make_uint4(pack_bf16(__uint_as_float(v[0]) * inv, __uint_as_float(v[1]) * inv),
+                              pack_bf16(__uint_as_float(v[2]) * inv, __uint_as_float(v[3]) * inv),
+                              pack_bf16(__uint_as_float(v[4]) * inv, __uint_as_float(v[5]) * inv),
+                              pack_bf16(__uint_as_float(v[6]) * inv, __uint_as_float(v[7]) * inv));
+        uint4 u1 = make_uint4(pack_bf16(__uint_as_float(v[8]) * inv, __uint_as_float(v[9]) * inv),
+                              pack_bf16(__uint_as_float(v[10]) * inv, __uint_as_float(v[11]) * inv),
+                              pack_bf16(__uint_as_float(v[12]) * inv, __uint_as_float(v[13]) * inv),
+                              pack_bf16(__uint_as_float(v[14]) * inv, __uint_as_float(v[15]) * inv));
+        *reinterpret_cast<uint4*>(orow + c * 16) = u0;
+        *reinterpret_cast<uint4*>(orow + c * 16 + 8) = u1;
+      }
+      if (valid) p.lse[static_cast<int64_t>(head) * p.n + row] = (m + log2f(l)) * 0.69314718055994531f;
     }
-    if (valid) p.lse[static_cast<int64_t>(head) * p.n + row] = (m + log2f(l)) * 0.69314718055994531f;
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -563,41 +641,6 @@ constexpr size_t dq_smem() {
 __device__ __forceinline__ void trace_mark(const AttnBwdParams& p, int ev, int it) {
   // every lane stores the same stamp: no lane-divergent branch in the MMA warp
   if (p.trace && it < 64 && blockIdx.x == gridDim.x - 1 && blockIdx.y == 0) p.trace[ev * 64 + it] = clock64();
-}
-
-// Copy this lane's [HD] bf16 row (`src`, or zeros when !valid) into TMEM as an
-// MMA A operand: column c of the lane holds elements (2c, 2c+1).
-template <int HD>
-__device__ __forceinline__ void row_to_tmem(uint32_t taddr, const __nv_bfloat16* src, bool valid) {
-  uint32_t v[HD / 2];
-#pragma unroll
-  for (int c = 0; c < HD / 8; ++c) {
-    const uint4 u = valid ? __ldg(reinterpret_cast<const uint4*>(src) + c) : make_uint4(0, 0, 0, 0);
-    v[4 * c] = u.x;
-    v[4 * c + 1] = u.y;
-    v[4 * c + 2] = u.z;
-    v[4 * c + 3] = u.w;
-  }
-#pragma unroll
-  for (int c = 0; c < HD / 16; ++c) tc::tmem_st8(taddr + 8 * c, v + 8 * c);
-}
-
-// Same for half of the row: elements [0, HD/2) of `src` -> HD/4 columns at taddr.
-template <int HD>
-__device__ __forceinline__ void row_part_to_tmem(uint32_t taddr, const __nv_bfloat16* src, bool valid) {
-  constexpr int NC = HD / 4;  // 32-bit columns (bf16 pairs): 20 (hd 80) / 16 (hd 64) / 32 (hd 128)
-  uint32_t v[NC];
-#pragma unroll
-  for (int c = 0; c < NC / 4; ++c) {
-    const uint4 u = valid ? __ldg(reinterpret_cast<const uint4*>(src) + c) : make_uint4(0, 0, 0, 0);
-    v[4 * c] = u.x;
-    v[4 * c + 1] = u.y;
-    v[4 * c + 2] = u.z;
-    v[4 * c + 3] = u.w;
-  }
-#pragma unroll
-  for (int c = 0; c + 8 <= NC; c += 8) tc::tmem_st8(taddr + c, v + c);
-  if constexpr (NC % 8 == 4) tc::tmem_st4(taddr + NC - 4, v + NC - 4);
 }
 
 // dK/dV: one CTA per (128-key block, head), looping over 64-query blocks that
@@ -1137,6 +1180,7 @@ void attn_fwd_tc(const void* q, const void* kv, void* o, float* lse, int64_t n, 
   make_maps(&p.tq, q, h, n, hd, 128);
   make_maps(&p.tkv, kv, 2 * h, kv_len, hd, 128);
   p.o = static_cast<__nv_bfloat16*>(o);
+  p.q = static_cast<const __nv_bfloat16*>(q);
   p.lse = lse;
   p.n = n;
   p.q_off = q_off;
@@ -1149,8 +1193,8 @@ void attn_fwd_tc(const void* q, const void* kv, void* o, float* lse, int64_t n, 
     constexpr size_t smem = fwd_smem<HD>();
     static_assert(smem <= 232448, "attention fwd smem");
     SPK_CUDA(cudaFuncSetAttribute(attn_fwd_tc_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 grid(static_cast<unsigned>((n + BQ - 1) / BQ), static_cast<unsigned>(H));
-    attn_fwd_tc_k<HD><<<grid, 256, smem, s>>>(p);
+    dim3 grid(static_cast<unsigned>(((n + BQ - 1) / BQ + 1) / 2), static_cast<unsigned>(H));  // query-tile pairs
+    attn_fwd_tc_k<HD><<<grid, 384, smem, s>>>(p);
     SPK_LAUNCH_CHECK();
   };
   switch (hd) {

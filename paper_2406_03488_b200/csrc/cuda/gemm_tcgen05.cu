@@ -13,6 +13,7 @@
 // all run on this one kernel without transposes.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "cuda/common.cuh"
@@ -246,6 +247,191 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_k(const __grid_constan
   if (warp == 1) tc::tmem_dealloc(tmem_base, TMEM_COLS);
 }
 
+// ----------------------------------------------------------------------------
+// 2-CTA (cta_group::2) variant: a CTA pair computes a 256x256 output tile with
+// tcgen05.mma.cta_group::2 (M = 256 split 128 per CTA, N = 256 with each CTA
+// holding half of the B tile). Per CTA and 64-wide K block the TMA brings
+// 16 KB of A + 16 KB of B (vs 48 KB for the 1-CTA 128x256 tile): the L2 ->
+// SMEM traffic per FLOP drops by a third, which is what bounds the 1-CTA
+// kernel (~16 TB/s of L2 reads at 1.4 PFLOP/s). The leader CTA (rank 0) issues
+// the MMAs; both CTAs load their halves with .cta_group::2 TMA completing on
+// the leader's barrier, and both drain their own TMEM rows in the epilogue.
+constexpr int BM2 = 128, BNH = 128, BK2 = 64, ST2 = 6;
+constexpr int A2_BYTES = BM2 * BK2 * 2, B2_BYTES = BNH * BK2 * 2, STAGE2_BYTES = A2_BYTES + B2_BYTES;
+constexpr int SMEM2_BYTES = ST2 * STAGE2_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t mapa_rank0(uint32_t saddr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_2cta(uint32_t dst, const CUtensorMap* m, uint32_t bar_cluster, int32_t c0,
+                                                 int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+template <typename TC>
+__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc2_k(const __grid_constant__ TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + ST2 * A2_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + ST2 * B2_BYTES);  // [ST2] used in the leader
+  uint64_t* empty = full + ST2;                                         // [ST2] both CTAs
+  uint64_t* tfull = empty + ST2;                                        // [2]   both CTAs
+  uint64_t* tempty = tfull + 2;                                         // [2]   used in the leader
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = tc::cluster_ctarank();
+  const int cid = static_cast<int>(blockIdx.x >> 1), ncl = static_cast<int>(gridDim.x >> 1);
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < ST2; ++s) {
+      tc::mbar_init(&full[s], 1);   // leader's arrive.expect_tx (both CTAs' bytes)
+      tc::mbar_init(&empty[s], 1);  // leader's multicast MMA commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  const int num_tiles = p.num_m_blk * p.num_n_blk;  // 256 x 256 tiles
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch(&p.tma_a);
+      tc::tma_prefetch(&p.tma_b);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
+        const int m0 = mb * 256 + static_cast<int>(rank) * BM2, n0 = nb * 256 + static_cast<int>(rank) * BNH;
+        for (int kb = 0; kb < p.num_k_blk; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t bar = mapa_rank0(tc::smem_u32(&full[stage]));
+          if (rank == 0) tc::mbar_expect_tx(&full[stage], 2 * STAGE2_BYTES);
+          const uint32_t a_dst = tc::smem_u32(sA + stage * A2_BYTES), b_dst = tc::smem_u32(sB + stage * B2_BYTES);
+          if (!p.a_mn) {
+            tma_load_2d_2cta(a_dst, &p.tma_a, bar, kb * BK2, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM2 / 64; ++j) tma_load_2d_2cta(a_dst + j * 8192, &p.tma_a, bar, m0 + 64 * j, kb * BK2);
+          }
+          if (!p.b_mn) {
+            tma_load_2d_2cta(b_dst, &p.tma_b, bar, kb * BK2, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BNH / 64; ++j) tma_load_2d_2cta(b_dst + j * 8192, &p.tma_b, bar, n0 + 64 * j, kb * BK2);
+          }
+          if (++stage == ST2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {  // leader issues for the pair (whole warp converged; elect inside the asm)
+      const uint32_t idesc = tc::idesc_bf16(256, 256, p.a_mn, p.b_mn);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        tc::mbar_wait_w(&tempty[acc], acc_phase ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem_base + acc * 256;
+        for (int kb = 0; kb < p.num_k_blk; ++kb) {
+          tc::mbar_wait_w(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t a_base = tc::smem_u32(sA + stage * A2_BYTES), b_base = tc::smem_u32(sB + stage * B2_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK2 / 16; ++kk) {
+            const uint64_t ad = p.a_mn ? tc::smem_desc(a_base + kk * 2048, 8192, 1024, tc::kSwizzle128B)
+                                       : tc::smem_desc(a_base + kk * 32, 16, 1024, tc::kSwizzle128B);
+            const uint64_t bd = p.b_mn ? tc::smem_desc(b_base + kk * 2048, 8192, 1024, tc::kSwizzle128B)
+                                       : tc::smem_desc(b_base + kk * 32, 16, 1024, tc::kSwizzle128B);
+            const uint32_t accum = (kb | kk) != 0;
+            asm volatile(
+                "{\n\t.reg .pred p, e;\n\t"
+                "elect.sync _|e, 0xffffffff;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                "l"(ad), "l"(bd), "r"(idesc), "r"(accum)
+                : "memory");
+          }
+          asm volatile(  // frees the stage in both CTAs once these MMAs retire
+              "{\n\t.reg .pred e;\n\t"
+              "elect.sync _|e, 0xffffffff;\n\t"
+              "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+                  tc::smem_u32(&empty[stage])),
+              "h"(static_cast<uint16_t>(3))
+              : "memory");
+          if (++stage == ST2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        asm volatile(
+            "{\n\t.reg .pred e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+                tc::smem_u32(&tfull[acc])),
+            "h"(static_cast<uint16_t>(3))
+            : "memory");
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int quarter = warp % 4;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cid; tile < num_tiles; tile += ncl) {
+      const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
+      tc::mbar_wait(&tfull[acc], acc_phase);
+      tc::tc_fence_after();
+      const int64_t row = (int64_t)mb * 256 + rank * BM2 + quarter * 32 + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 256; c0 += 32) {
+        const int64_t col0 = (int64_t)nb * 256 + c0;
+        uint32_t r[32];
+        tc::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 256 + c0, r);
+        tc::tmem_ld_wait();
+        if (row < p.g.M && col0 < p.g.N) store_chunk<TC>(p.g, row, col0, r);
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(mapa_rank0(tc::smem_u32(&tempty[acc])));
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS) : "memory");
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -291,6 +477,13 @@ bool gemm_tc_supported(const GemmArgs& a) {
 
 void gemm_tcgen05(const GemmArgs& a, cudaStream_t s) {
   if (!gemm_tc_supported(a)) throw std::invalid_argument("gemm_tcgen05: unsupported operand layout/alignment");
+  static const int force = [] {
+    const char* e = std::getenv("SP_GEMM_CTA");  // tuning: 1 = force the 1-CTA kernel, 2 = force 2-CTA
+    return e ? std::atoi(e) : 0;
+  }();
+  // 2-CTA 256x256 tiles once the problem has enough of them to fill the pairs.
+  const int64_t tiles2 = ((a.M + 255) / 256) * ((a.N + 255) / 256);
+  const bool two = force == 2 || (force != 1 && tiles2 >= num_sms() / 2);
   TcParams p;
   p.g = a;
   p.a_mn = !a.a_kmajor;
@@ -299,10 +492,37 @@ void gemm_tcgen05(const GemmArgs& a, cudaStream_t s) {
     make_map(&p.tma_a, a.A, a.K, a.M, a.lda, 64, BM);
   else
     make_map(&p.tma_a, a.A, a.M, a.K, a.lda, 64, 64);
+  const uint32_t bn_box = two ? BNH : BN;
   if (a.b_kmajor)
-    make_map(&p.tma_b, a.B, a.K, a.N, a.ldb, 64, BN);
+    make_map(&p.tma_b, a.B, a.K, a.N, a.ldb, 64, bn_box);
   else
     make_map(&p.tma_b, a.B, a.N, a.K, a.ldb, 64, 64);
+  if (two) {
+    p.num_m_blk = static_cast<int>((a.M + 255) / 256);
+    p.num_n_blk = static_cast<int>((a.N + 255) / 256);
+    p.num_k_blk = static_cast<int>((a.K + BK2 - 1) / BK2);
+    const int pairs = static_cast<int>(tiles2 < num_sms() / 2 ? tiles2 : num_sms() / 2);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(2 * pairs);
+    lc.blockDim = dim3(NUM_THREADS);
+    lc.dynamicSmemBytes = SMEM2_BYTES;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    if (a.c == DType::kF32) {
+      SPK_CUDA(cudaFuncSetAttribute(gemm_tc2_k<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
+      SPK_CUDA(cudaLaunchKernelEx(&lc, gemm_tc2_k<float>, p));
+    } else {
+      SPK_CUDA(cudaFuncSetAttribute(gemm_tc2_k<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
+      SPK_CUDA(cudaLaunchKernelEx(&lc, gemm_tc2_k<__nv_bfloat16>, p));
+    }
+    return;
+  }
   p.num_m_blk = static_cast<int>((a.M + BM - 1) / BM);
   p.num_n_blk = static_cast<int>((a.N + BN - 1) / BN);
   p.num_k_blk = static_cast<int>((a.K + BK - 1) / BK);
