@@ -65,12 +65,22 @@ int sp_attention_bwd(int32_t dtype, int32_t impl, const void* q, const void* kv,
                      int32_t head_dim, void* stream) {
   return cuda_guard([&] {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    float* ws = nullptr;
+    // Workspace cached per device and grown on demand (a per-call cudaMallocAsync /
+    // cudaFreeAsync pair returns memory to the driver at every sync and distorts timing).
+    static thread_local float* ws_buf[64] = {};
+    static thread_local size_t ws_cap[64] = {};
+    int dev = 0;
+    SPK_CUDA(cudaGetDevice(&dev));
     const size_t floats = spk::attn_bwd_ws_delta_floats(n, heads) + static_cast<size_t>(n) * heads * head_dim;
-    SPK_CUDA(cudaMallocAsync(&ws, floats * sizeof(float), s));
+    if (dev < 0 || dev >= 64) throw std::invalid_argument("device ordinal out of range");
+    if (ws_cap[dev] < floats) {
+      if (ws_buf[dev]) SPK_CUDA(cudaFree(ws_buf[dev]));
+      SPK_CUDA(cudaMalloc(&ws_buf[dev], floats * sizeof(float)));
+      ws_cap[dev] = floats;
+    }
+    float* ws = ws_buf[dev];
     spk::attn_bwd(dt(dtype), impl, q, kv, o, dout, lse, ws, ws + spk::attn_bwd_ws_delta_floats(n, heads), dq, dkv_acc, n, q_off,
                   kv_len, heads, head_dim, s);
-    SPK_CUDA(cudaFreeAsync(ws, s));
   });
 }
 

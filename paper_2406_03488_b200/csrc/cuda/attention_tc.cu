@@ -281,7 +281,8 @@ struct FwdCfg {
 
 template <int HD>
 constexpr size_t fwd_smem_n(int st) {
-  return (FwdCfg<HD>::QT ? 0 : 2 * Lay<HD>::bytes(128)) + 2 * st * Lay<HD>::bytes(128) + (16 + 4 * st) * 8 + 8 + 1024;
+  return (FwdCfg<HD>::QT ? 0 : 2 * Lay<HD>::bytes(128)) + 2 * st * Lay<HD>::bytes(128) + (16 + 4 * st) * 8 + 16 +
+         2 * 2 * 2 * 128 * 4 + 1024;  // + softmax row-max / row-sum exchange
 }
 // Ring depths: as many K / V stages as the opt-in SMEM (227 KB) holds, capped at 6.
 template <int HD>
@@ -298,7 +299,7 @@ constexpr size_t fwd_smem() {
 // ============================================================================ forward
 
 template <int HD>
-__global__ void __launch_bounds__(384, 1) attn_fwd_tc_k(const __grid_constant__ AttnParams p) {
+__global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ AttnParams p) {
   using C = FwdCfg<HD>;
   constexpr int KVS = fwd_stages<HD>();
   constexpr int TB = Lay<HD>::bytes(128);
@@ -340,10 +341,10 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_k(const __grid_constant__ 
   const int nblk = nblk_t[0] > nblk_t[1] ? nblk_t[0] : nblk_t[1];
 
   if (threadIdx.x == 0) {
-    tc::mbar_init(q_ready, C::QT ? 8 : 1);  // softmax warps (TMEM copy) or the TMA
+    tc::mbar_init(q_ready, C::QT ? 16 : 1);  // softmax warps (TMEM copy) or the TMA
     for (int t = 0; t < 2; ++t) {
       tc::mbar_init(&s_full[t], 1);
-      tc::mbar_init(&p_full[t], 4);  // the tile's softmax warps
+      tc::mbar_init(&p_full[t], 8);  // the tile's softmax warps
       tc::mbar_init(&pv_done[t], 1);
     }
     for (int i = 0; i < KVS; ++i) {
@@ -426,18 +427,20 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_k(const __grid_constant__ 
         tc::mbar_wait_w(&p_full[t], j & 1);
         tc::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_nhd_ts<HD>(tmem + C::t_o(t), tmem + t * 128 + kk * 8, v_base, 128, kk, j > 0 || kk > 0);
+        for (int kk = 0; kk < BKV / 16; ++kk)  // P of keys [64hf, 64hf+64) is packed at columns [64hf, 64hf+32)
+          mma_nhd_ts<HD>(tmem + C::t_o(t), tmem + t * 128 + 64 * (kk >> 2) + 8 * (kk & 3), v_base, 128, kk,
+                         j > 0 || kk > 0);
         tc::mma_commit_w(&pv_done[t]);
       }
       tc::mma_commit_w(&v_empty[st]);
     }
   } else if (warp >= 4) {
-    // Softmax of tile t = (warp-4)/4, one query row per thread: S row in
-    // registers (one pass), P -> TMEM, O stays in TMEM. The running max used for
-    // exponentiation only moves when a block raises it by more than 2^8 (log2
-    // domain); then the O row in TMEM is rescaled once PV_t(j-1) has landed.
-    const int t = (warp - 4) >> 2, quarter = warp & 3;
+    // 16 softmax warps: tile t = (w-4)/8, column half hf = ((w-4)/4)&1, TMEM lane
+    // quarter w%4 (one query row per lane). The two warps of a (tile, quarter)
+    // share their rows: each takes 64 of the block's 128 key columns, they swap
+    // row maxima through shared memory (one 64-thread named barrier per block)
+    // and keep partial row sums that are combined once at the end.
+    const int sw = warp - 4, t = sw >> 3, hf = (sw >> 2) & 1, quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const int64_t row = q0_t[t] + r;
     const bool valid = nblk_t[t] > 0 && row < p.n;
@@ -445,37 +448,41 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_k(const __grid_constant__ 
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t obase = tmem + lane_base + C::t_o(t);
     const int nb = nblk_t[t];
-    if constexpr (C::QT) {
-      row_to_tmem<HD>(tmem + lane_base + C::t_q(t), p.q + (valid ? row : 0) * p.h + head * HD, valid);
+    const int bar_id = 1 + t * 4 + quarter;  // named barrier of this row group's two warps
+    float* xch = reinterpret_cast<float*>(tmem_slot + 4);  // [2 parity][2 tiles][2 halves][128 rows]
+    if constexpr (C::QT) {  // each half copies half of this lane's Q row
+      row_part_to_tmem<HD>(tmem + lane_base + C::t_q(t) + hf * (HD / 4),
+                           p.q + (valid ? row : 0) * p.h + head * HD + hf * (HD / 2), valid);
       tc::tmem_st_wait();
       tc::tc_fence_before();
       warp_arrive(q_ready);
     }
+    constexpr int NCH = HD / 16, SPLIT = (NCH + 1) / 2;  // O column chunks owned by half 0 / half 1
+    const int c_begin = hf ? SPLIT : 0, c_end = hf ? NCH : SPLIT;
     constexpr float kRescale = 8.f;
     float m = -INFINITY, l = 0.f;
 
     for (int j = 0; j < nb; ++j) {
-      const int64_t lim64 = (valid ? (qpos < p.kv_len - 1 ? qpos : p.kv_len - 1) : -1) - static_cast<int64_t>(j) * BKV;
-      const int lim = lim64 > 1000000 ? 1000000 : static_cast<int>(lim64);  // columns <= lim are visible
+      const int64_t lim64 =
+          (valid ? (qpos < p.kv_len - 1 ? qpos : p.kv_len - 1) : -1) - static_cast<int64_t>(j) * BKV - 64 * hf;
+      const int lim = lim64 > 1000000 ? 1000000 : static_cast<int>(lim64);  // local columns <= lim are visible
       tc::mbar_wait(&s_full[t], j & 1);
       tc::tc_fence_after();
-      const uint32_t sbase = tmem + lane_base + t * 128;
-      uint32_t sv[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tc::tmem_ld32(sbase + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
+      const uint32_t sbase = tmem + lane_base + t * 128 + 64 * hf;
+      uint32_t sv[64];
+      tc::tmem_ld32(sbase, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+      tc::tmem_ld32(sbase + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
       tc::tmem_ld_wait();
-      // Raw scores stay unscaled (scale > 0 commutes with max); masking only on
-      // blocks that touch the causal diagonal or the prefix end.
-      if (!__all_sync(0xffffffffu, lim >= BKV - 1)) {
+      if (!__all_sync(0xffffffffu, lim >= 63)) {
 #pragma unroll
-        for (int c = 0; c < 128; ++c)
+        for (int c = 0; c < 64; ++c)
           if (c > lim) sv[c] = __float_as_uint(-INFINITY);
       }
       float mx;
-      {  // four independent FMNMX3 chains
+      {
         float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 128; c += 8) {
+        for (int c = 0; c < 64; c += 8) {
           m0 = fmax3(m0, __uint_as_float(sv[c]), __uint_as_float(sv[c + 1]));
           m1 = fmax3(m1, __uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3]));
           m2 = fmax3(m2, __uint_as_float(sv[c + 4]), __uint_as_float(sv[c + 5]));
@@ -483,17 +490,22 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_k(const __grid_constant__ 
         }
         mx = fmax3(m0, m1, fmaxf(m2, m3));
       }
+      {  // row max over both halves (parity-buffered slots: one barrier per block)
+        float* slot = xch + (((j & 1) * 2 + t) * 2) * 128;
+        slot[hf * 128 + r] = mx;
+        tc::named_bar_sync(bar_id, 64);
+        mx = fmaxf(mx, slot[(hf ^ 1) * 128 + r]);
+      }
       mx *= p.scale_log2;
       const bool need = (m == -INFINITY) ? (mx > -INFINITY || j == 0) : (mx > m + kRescale);
       if (__any_sync(0xffffffffu, need)) {
         const float m_new = need ? fmaxf(m, mx) : m;
         const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
-        if (j > 0) {  // rescale the O row accumulated so far (PV_t(j-1) must have landed)
+        if (j > 0) {  // rescale this half's O columns (PV_t(j-1) must have landed)
           // pv_done[t] cannot be past phase j-1 here: PV_t(j) needs this P_t(j).
           tc::mbar_wait(&pv_done[t], (j - 1) & 1);
           tc::tc_fence_after();
-#pragma unroll
-          for (int c = 0; c < HD / 16; ++c) {
+          for (int c = c_begin; c < c_end; ++c) {
             uint32_t v[16];
             tmem_ld16(obase + c * 16, v);
             tc::tmem_ld_wait();
@@ -510,7 +522,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_k(const __grid_constant__ 
       const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(neg_m, neg_m);
       float2 rs_a = make_float2(0.f, 0.f), rs_b = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t w[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
@@ -522,7 +534,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_k(const __grid_constant__ 
           w[e / 2] = pack2(x0);
           w[e / 2 + 1] = pack2(x1);
         }
-        tc::tmem_st16(sbase + c * 16, w);  // P keys [32c, 32c+32) -> columns [16c, 16c+16)
+        tc::tmem_st16(sbase + c * 16, w);  // P keys [64hf + 32c, +32) -> columns [64hf + 16c, +16)
       }
       l += (rs_a.x + rs_a.y) + (rs_b.x + rs_b.y);
       tc::tmem_st_wait();
@@ -530,12 +542,17 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_k(const __grid_constant__ 
       warp_arrive(&p_full[t]);
     }
     if (nb > 0) {
+      {  // combine the two halves' partial row sums
+        float* slot = xch + (((nb & 1) * 2 + t) * 2) * 128;
+        slot[hf * 128 + r] = l;
+        tc::named_bar_sync(bar_id, 64);
+        l += slot[(hf ^ 1) * 128 + r];
+      }
       tc::mbar_wait(&pv_done[t], (nb - 1) & 1);  // last PV_t landed
       tc::tc_fence_after();
       const float inv = l > 0.f ? 1.f / l : 0.f;
       __nv_bfloat16* orow = p.o + (valid ? row : 0) * p.h + head * HD;
-#pragma unroll
-      for (int c = 0; c < HD / 16; ++c) {
+      for (int c = c_begin; c < c_end; ++c) {
         uint32_t v[16];
         tmem_ld16(obase + c * 16, v);  // warp-collective
         tc::tmem_ld_wait();
@@ -551,7 +568,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_k(const __grid_constant__ 
         *reinterpret_cast<uint4*>(orow + c * 16) = u0;
         *reinterpret_cast<uint4*>(orow + c * 16 + 8) = u1;
       }
-      if (valid) p.lse[static_cast<int64_t>(head) * p.n + row] = (m + log2f(l)) * 0.69314718055994531f;
+      if (valid && hf == 0) p.lse[static_cast<int64_t>(head) * p.n + row] = (m + log2f(l)) * 0.69314718055994531f;
     }
   }
   tc::tc_fence_before();
@@ -1194,7 +1211,7 @@ void attn_fwd_tc(const void* q, const void* kv, void* o, float* lse, int64_t n, 
     static_assert(smem <= 232448, "attention fwd smem");
     SPK_CUDA(cudaFuncSetAttribute(attn_fwd_tc_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid(static_cast<unsigned>(((n + BQ - 1) / BQ + 1) / 2), static_cast<unsigned>(H));  // query-tile pairs
-    attn_fwd_tc_k<HD><<<grid, 384, smem, s>>>(p);
+    attn_fwd_tc_k<HD><<<grid, 640, smem, s>>>(p);
     SPK_LAUNCH_CHECK();
   };
   switch (hd) {
