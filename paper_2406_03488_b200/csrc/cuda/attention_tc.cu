@@ -625,7 +625,7 @@ struct DqCfg {
 
 template <int HD>
 constexpr size_t dkv_smem_n(int st) {
-  return (DkvCfg<HD>::KVT ? 0 : 2 * Lay<HD>::bytes(128)) + 2 * st * Lay<HD>::bytes(64) + st * 512 + (16 + 2 * st) * 8 +
+  return (DkvCfg<HD>::KVT ? 0 : 2 * Lay<HD>::bytes(128)) + 2 * st * Lay<HD>::bytes(64) + st * 512 + (20 + 2 * st) * 8 +
          8 + 1024;
 }
 template <int HD>
@@ -640,7 +640,7 @@ constexpr size_t dkv_smem() {
 }
 template <int HD>
 constexpr size_t dq_smem_n(int st) {
-  return 2 * st * Lay<HD>::bytes(64) + (16 + 2 * st) * 8 + 8 + 1024;
+  return 2 * st * Lay<HD>::bytes(64) + (20 + 2 * st) * 8 + 8 + 1024;
 }
 template <int HD>
 constexpr int dq_stages() {
@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
   uint64_t* dp_free = bars + 10;  // [ND]  dP^T_i loaded into registers (buffer reusable)
   uint64_t* q_full = bars + 12;          // [QST]
   uint64_t* q_empty = q_full + QST;      // [QST]
-  uint64_t* s_free = q_empty + QST;      // [NS]  dV/dK_i completed: S buffer i % NS reusable
+  uint64_t* s_free = q_empty + QST;      // [NS]  dV/dK_i completed: score buffer i % NS reusable
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + NS);
 
   // 2-CTA cluster: CTAs own adjacent 128-key blocks and stream the same query
@@ -757,41 +757,52 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
         tc::bulk_load(sLD + st * 128, p.ld + (static_cast<int64_t>(head) * p.n_pad + i0) * 2, 512, &q_full[st]);
       }
     }
-  } else if (warp == 1 || warp == 2) {
-    // Two MMA-issuing warps (whole warp converged; tc::*_w elect the issuing
-    // lane). A tcgen05.mma issue returns only about when the tensor pipe takes
-    // it, so every cycle an issuing warp spends waiting on a barrier is a pipe
-    // bubble; with S/dP on warp 1 and dV/dK on warp 2, one warp's waits are
-    // covered by the other's issue. Cross-warp TMEM reuse is ordered by
-    // barriers (s_free: dV/dK_i completed), not by issue order.
+  } else if (warp >= 1 && warp <= 3) {
+    // Three MMA-issuing warps (whole warp converged; tc::*_w elect the issuing
+    // lane): warp 1 dP^T, warp 2 dV/dK, warp 3 S^T. A tcgen05.mma issue returns
+    // only about when the tensor pipe takes it, so every cycle an issuing warp
+    // spends on a barrier wait or commit is a pipe bubble unless another warp
+    // has MMAs ready; S^T reuse of a score buffer waits for dV/dK of the block
+    // that read it (s_free).
     constexpr uint32_t idesc_s = tc::idesc_bf16(128, 64, false, false);
     tc::mbar_wait_w(kv_full, 0);
     tc::tc_fence_after();
-    if (warp == 1) {
-      const uint32_t k_base = tc::smem_u32(sK), v_base = tc::smem_u32(sV);
-      // S^T = K Q^T / dP^T = V dO^T: A = K / V (TMEM copy, or SMEM tile for hd 128).
-      auto kv_mma = [&](uint32_t d, uint32_t t_a, uint32_t a_base, uint32_t b_base) {
+    const uint32_t k_base = tc::smem_u32(sK), v_base = tc::smem_u32(sV);
+    // S^T = K Q^T / dP^T = V dO^T: A = K / V (TMEM copy, or SMEM tile for hd 128).
+    auto kv_mma = [&](uint32_t d, uint32_t t_a, uint32_t a_base, uint32_t b_base) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          if constexpr (C::KVT)
-            tc::mma_bf16_ts_w(d, tmem + t_a + 8 * kk, kdesc<HD>(b_base, 64, kk), idesc_s, kk > 0);
-          else
-            tc::mma_bf16_ss_w(d, kdesc<HD>(a_base, 128, kk), kdesc<HD>(b_base, 64, kk), idesc_s, kk > 0);
-        }
-      };
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        if constexpr (C::KVT)
+          tc::mma_bf16_ts_w(d, tmem + t_a + 8 * kk, kdesc<HD>(b_base, 64, kk), idesc_s, kk > 0);
+        else
+          tc::mma_bf16_ss_w(d, kdesc<HD>(a_base, 128, kk), kdesc<HD>(b_base, 64, kk), idesc_s, kk > 0);
+      }
+    };
+    auto issue_s = [&](int it) {  // S^T_it into score buffer it % NS
+      const int st = it % QST;
+      tc::mbar_wait_w(&q_full[st], (it / QST) & 1);
+      tc::tc_fence_after();
+      if (!(p.dbg & 1)) kv_mma(tmem + (it % NS) * 64, C::T_K, k_base, tc::smem_u32(sQ + st * Q_T));
+      tc::mma_commit_w(&s_full[it % NS]);
+      trace_mark(p, 3, it);
+    };
+    if (warp == 1) {
+      // dP^T issuer: dP^T_it as soon as the softmax has loaded dP^T_{it-ND} (its
+      // buffer) -- the dP path is the one the softmax waits on, so it gets a warp
+      // of its own with a single wait per block.
       for (int it = 0; it < niter; ++it) {
-        const int b = it % NS, st = it % QST;
+        const int st = it % QST;
         tc::mbar_wait_w(&q_full[st], (it / QST) & 1);
-        if (it >= NS) tc::mbar_wait_w(&s_free[b], ((it / NS) - 1) & 1);  // dV/dK of it-NS read buffer b
-        tc::tc_fence_after();
-        if (!(p.dbg & 1)) kv_mma(tmem + b * 64, C::T_K, k_base, tc::smem_u32(sQ + st * Q_T));
-        tc::mma_commit_w(&s_full[b]);
-        trace_mark(p, 3, it);
-        if (it >= ND) tc::mbar_wait_w(&dp_free[it % ND], ((it / ND) - 1) & 1);  // softmax loaded dP^T_{it-ND}
+        if (it >= ND) tc::mbar_wait_w(&dp_free[it % ND], ((it / ND) - 1) & 1);
         tc::tc_fence_after();
         if (!(p.dbg & 1)) kv_mma(tmem + C::T_DP + (it % ND) * 64, C::T_V, v_base, tc::smem_u32(sdO + st * Q_T));
         tc::mma_commit_w(&dp_full[it % ND]);
         trace_mark(p, 2, it);
+      }
+    } else if (warp == 3) {
+      for (int it = 0; it < niter; ++it) {
+        if (it >= NS) tc::mbar_wait_w(&s_free[it % NS], ((it / NS) - 1) & 1);
+        issue_s(it);
       }
     } else {
       for (int it = 0; it < niter; ++it) {
@@ -1011,32 +1022,41 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dq_k(const __grid_constant__ 
         load_tile<HD>(sV + st * K_T, p.tkv, &kv_full[st], p.h + head * HD, j * 64, 64, 0);
       }
     }
-  } else if (warp == 1 || warp == 2) {
-    // Two MMA-issuing warps (see the dK/dV kernel): warp 1 issues S_j / dP_j,
-    // warp 2 issues dQ += dS_j K_j; score-buffer reuse is ordered by s_free.
+  } else if (warp >= 1 && warp <= 3) {
+    // Three MMA-issuing warps (see the dK/dV kernel): warp 1 dP_j, warp 2
+    // dQ += dS_j K_j, warp 3 S_j (after dQ_{j-NS} released its score buffer).
     constexpr uint32_t idesc_s = tc::idesc_bf16(128, 64, false, false);
     tc::mbar_wait_w(qo_full, 0);
     tc::tc_fence_after();
-    if (warp == 1) {
-      for (int j = 0; j < nblk; ++j) {
-        const int b = j % NS, st = j % KST;
-        tc::mbar_wait_w(&kv_full[st], (j / KST) & 1);
-        if (j >= NS) tc::mbar_wait_w(&s_free[b], ((j / NS) - 1) & 1);  // dQ_{j-NS} read buffer b
-        tc::tc_fence_after();
-        const uint32_t k_base = tc::smem_u32(sK + st * K_T), v_base = tc::smem_u32(sV + st * K_T);
+    auto issue_s = [&](int j) {  // S_j into score buffer j % NS
+      const int st = j % KST;
+      tc::mbar_wait_w(&kv_full[st], (j / KST) & 1);
+      tc::tc_fence_after();
+      const uint32_t k_base = tc::smem_u32(sK + st * K_T);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          tc::mma_bf16_ts_w(tmem + b * 64, tmem + C::T_Q + 8 * kk, kdesc<HD>(k_base, 64, kk), idesc_s, kk > 0);
-        tc::mma_commit_w(&s_full[b]);
+      for (int kk = 0; kk < HD / 16; ++kk)
+        tc::mma_bf16_ts_w(tmem + (j % NS) * 64, tmem + C::T_Q + 8 * kk, kdesc<HD>(k_base, 64, kk), idesc_s, kk > 0);
+      tc::mma_commit_w(&s_full[j % NS]);
+    };
+    if (warp == 1) {  // dP issuer (see the dK/dV kernel)
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j % KST;
+        tc::mbar_wait_w(&kv_full[st], (j / KST) & 1);
         if (j >= ND) tc::mbar_wait_w(&dp_free[j % ND], ((j / ND) - 1) & 1);  // softmax loaded dP_{j-ND}
         tc::tc_fence_after();
+        const uint32_t v_base = tc::smem_u32(sV + st * K_T);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
           tc::mma_bf16_ts_w(tmem + C::T_DP + (j % ND) * 64, tmem + C::T_DO + 8 * kk, kdesc<HD>(v_base, 64, kk), idesc_s,
                             kk > 0);
         tc::mma_commit_w(&dp_full[j % ND]);
       }
-    } else {
+    } else if (warp == 3) {
+      for (int j = 0; j < nblk; ++j) {
+        if (j >= NS) tc::mbar_wait_w(&s_free[j % NS], ((j / NS) - 1) & 1);
+        issue_s(j);
+      }
+    } else {  // dQ issuer
       for (int j = 0; j < nblk; ++j) {
         const int b = j % NS, st = j % KST;
         tc::mbar_wait_w(&ds_full[b], (j / NS) & 1);
@@ -1045,7 +1065,9 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dq_k(const __grid_constant__ 
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // K = 64 keys
           mma_nhd_ts<HD>(tmem + C::T_DQ, tmem + b * 64 + 16 * kk, k_base, 64, kk, j > 0 || kk > 0);
-        tc::mma_commit_w(&kv_empty[st]);  // S_j / dP_j (also readers of the stage) completed before dS_j
+        // kv stage j is released after dQ_j AND dP_j (other warp): dP_j completed before
+        // the softmax could publish dS_j, so this commit covers every reader of the stage.
+        tc::mma_commit_w(&kv_empty[st]);
         tc::mma_commit_w(&s_free[b]);
       }
       tc::mma_commit_w(done);
