@@ -324,6 +324,27 @@ def main():
                     "modeled_bubble_ratio": float(r1.aggregate_bubble_ratio)}
     except Exception as e:  # pragma: no cover
         mem_1f1b = {"error": str(e)}
+    # Engine arena plan (host-side replay of each schedule's op order, KV-prefix slabs
+    # included) for Seq1F1B vs batch-level 1F1B of the same model at several pipeline
+    # depths: at depth 1 both schedules hold one micro-batch, the paper's memory claim is
+    # about depth > 1 (stage 1 holds P micro-batches under 1F1B).
+    memory_model = {}
+    for P in sorted({args.gpus, 4, 8}):
+        try:
+            Mp = cfg.micro_batches if P == args.gpus else (8 if P <= 4 else 2 * P)
+            cs = model_and_cfg(P, args.seq, Mp, args.k)[1]
+            c1 = model_and_cfg(P, args.seq, Mp, 1)[1]
+            ls, _, _ = E.plan_memory(cs, "seq1f1b", pl.cwp_partition(cs), model, stage=1)
+            l1, _, _ = E.plan_memory(c1, "1f1b", pl.even_partition(c1), model, stage=1)
+            rs = pl.simulate(pl.generate(cs, "seq1f1b", pl.cwp_partition(cs)), pl.cwp_partition(cs), with_series=False)
+            rb = pl.simulate(pl.generate(c1, "1f1b", pl.even_partition(c1)), pl.even_partition(c1), with_series=False)
+            memory_model[f"P{P}_M{Mp}"] = {
+                "seq1f1b_peak_activation_gb_stage1": ls / 1e9, "1f1b_peak_activation_gb_stage1": l1 / 1e9,
+                "ratio": ls / l1 if l1 else None,
+                "seq1f1b_modeled_bubble": float(rs.aggregate_bubble_ratio),
+                "1f1b_modeled_bubble": float(rb.aggregate_bubble_ratio)}
+        except Exception as e:  # pragma: no cover
+            memory_model[f"P{P}"] = {"error": str(e)}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -346,6 +367,7 @@ def main():
             "bubble_ratio": bubble, "modeled": modeled,
             "peak_activation_gb_per_stage": peak_act,
             "batch_level_1f1b": mem_1f1b,
+            "memory_model": memory_model,
             # Kernels timed inside a seconds-long step run under the power cap: the
             # denominator is the sustained bf16 figure (burst reported beside it).
             "roofline": {"bound": "tensor", "kernel": names[dom], "achieved": achieved, "peak": sustained,
