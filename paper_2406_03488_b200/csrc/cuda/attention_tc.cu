@@ -97,6 +97,15 @@ __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
   if ((threadIdx.x & 31) == 0) tc::mbar_arrive(bar);
 }
 
+__device__ __forceinline__ void sts_f32(const void* p, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "f"(v) : "memory");
+}
+__device__ __forceinline__ float lds_f32(const void* p) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ float4 lds_f4(const void* p) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -216,6 +225,9 @@ __device__ __forceinline__ float2 ex2x2_poly(float2 x) {
 // `poly` is a constant after the softmax loops are unrolled.
 __device__ __forceinline__ float2 ex2x2_sel(bool poly, float2 v) { return poly ? ex2x2_poly(v) : ex2x2(v); }
 // Which groups of a fully unrolled softmax loop use the FMA-pipe exponential: 3 of 8.
+#ifndef SPK_FWD_TURN
+#define SPK_FWD_TURN 0  // measured slower at hd 80 (variant sweep); forward tiles alternate their exponentials: 0 off, 1 before exp, 2 whole block
+#endif
 #ifndef SPK_POLY_FWD
 #define SPK_POLY_FWD 3
 #endif
@@ -313,6 +325,7 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
   uint64_t* s_full = bars + 1;   // [2 tiles]
   uint64_t* p_full = bars + 3;   // [2 tiles]  P packed into the tile's S buffer
   uint64_t* pv_done = bars + 5;  // [2 tiles]  O += P V completed
+  uint64_t* turn = bars + 7;     // [2 tiles]  tile t finished the exponentials of a block
   uint64_t* k_full = bars + 16;          // [KVS]
   uint64_t* k_empty = k_full + KVS;      // [KVS]
   uint64_t* v_full = k_empty + KVS;      // [KVS]
@@ -346,6 +359,7 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
       tc::mbar_init(&s_full[t], 1);
       tc::mbar_init(&p_full[t], 8);  // the tile's softmax warps
       tc::mbar_init(&pv_done[t], 1);
+      tc::mbar_init(&turn[t], 8);
     }
     for (int i = 0; i < KVS; ++i) {
       tc::mbar_init(&k_full[i], 1);
@@ -466,6 +480,8 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
       const int64_t lim64 =
           (valid ? (qpos < p.kv_len - 1 ? qpos : p.kv_len - 1) : -1) - static_cast<int64_t>(j) * BKV - 64 * hf;
       const int lim = lim64 > 1000000 ? 1000000 : static_cast<int>(lim64);  // local columns <= lim are visible
+      if (SPK_FWD_TURN == 2 && (t == 0 ? (j > 0 && j - 1 < nblk_t[1]) : (j < nblk_t[0])))
+        tc::mbar_wait(&turn[t ^ 1], t == 0 ? ((j - 1) & 1) : (j & 1));
       tc::mbar_wait(&s_full[t], j & 1);
       tc::tc_fence_after();
       const uint32_t sbase = tmem + lane_base + t * 128 + 64 * hf;
@@ -492,9 +508,9 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
       }
       {  // row max over both halves (parity-buffered slots: one barrier per block)
         float* slot = xch + (((j & 1) * 2 + t) * 2) * 128;
-        slot[hf * 128 + r] = mx;
+        sts_f32(slot + hf * 128 + r, mx);
         tc::named_bar_sync(bar_id, 64);
-        mx = fmaxf(mx, slot[(hf ^ 1) * 128 + r]);
+        mx = fmaxf(mx, lds_f32(slot + (hf ^ 1) * 128 + r));
       }
       mx *= p.scale_log2;
       const bool need = (m == -INFINITY) ? (mx > -INFINITY || j == 0) : (mx > m + kRescale);
@@ -518,6 +534,13 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
         l *= alpha;
         m = m_new;
       }
+      // The two tiles take turns on the exponentials (A(j), B(j), A(j+1), ...):
+      // the MUFU / issue slots then serve one tile at a time while the tensor pipe
+      // runs the other tile's PV and next S, instead of both softmaxes sharing the
+      // SM and finishing together. turn[u] cannot run two phases ahead of the
+      // waiter: each side waits for the other before its next block.
+      if (SPK_FWD_TURN == 1 && (t == 0 ? (j > 0 && j - 1 < nblk_t[1]) : (j < nblk_t[0])))
+        tc::mbar_wait(&turn[t ^ 1], t == 0 ? ((j - 1) & 1) : (j & 1));
       const float neg_m = m == -INFINITY ? 0.f : -m;
       const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(neg_m, neg_m);
       float2 rs_a = make_float2(0.f, 0.f), rs_b = make_float2(0.f, 0.f);
@@ -540,13 +563,14 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
       tc::tmem_st_wait();
       tc::tc_fence_before();
       warp_arrive(&p_full[t]);
+      if (SPK_FWD_TURN) warp_arrive(&turn[t]);
     }
     if (nb > 0) {
       {  // combine the two halves' partial row sums
         float* slot = xch + (((nb & 1) * 2 + t) * 2) * 128;
-        slot[hf * 128 + r] = l;
+        sts_f32(slot + hf * 128 + r, l);
         tc::named_bar_sync(bar_id, 64);
-        l += slot[(hf ^ 1) * 128 + r];
+        l += lds_f32(slot + (hf ^ 1) * 128 + r);
       }
       tc::mbar_wait(&pv_done[t], (nb - 1) & 1);  // last PV_t landed
       tc::tc_fence_after();
