@@ -20,6 +20,8 @@
  *   sp_dependencies                         core/include/seqpipe/sim.hpp:27, core/src/sim.cpp:14-44
  *   sp_simulate                             core/include/seqpipe/sim.hpp:80, core/src/sim.cpp:121-317
  *   sp_check_schedule / sp_check_warmup     core/include/seqpipe/validate.hpp:34,42, core/src/validate.cpp:85-325
+ *   sp_schedule_to_json / _from_json        core/include/seqpipe/json_io.hpp:19-20, core/src/json_io.cpp:59-97
+ *   sp_report_to_json                       core/include/seqpipe/json_io.hpp:25-26, core/src/json_io.cpp:99-159
  *   sp_device_partition / sp_device_schedule_ops   GPU-resident launcher core (no reference counterpart;
  *                                           bit-exact with cwp_partition/generate)
  *   sp_engine_*                             replaces the modeled execution of simulate() (sim.cpp:121-317)
@@ -183,6 +185,19 @@ int sp_simulate_memory_series(const sp_scenario* cfg, int32_t kind, const int64_
                               const sp_task* ops, const int64_t* counts, int32_t device,
                               sp_rational* series, int64_t* len);
 
+/* ---- JSON wire formats (core/include/seqpipe/json_io.hpp:19-26, core/src/json_io.cpp:59-159) ----
+ * seqpipe.schedule.v1 of an op table / seqpipe.simreport.v1 of its simulation, canonical bytes
+ * (sorted keys, exact rationals, `indent` spaces per level, trailing newline). Text out via
+ * (buf, len): buf == NULL returns the needed size (incl. NUL) in *len. sp_schedule_from_json:
+ * ops == NULL fills cfg_out / kind_out / counts[P] only (P <= max_devices). */
+int sp_schedule_to_json(const sp_scenario* cfg, int32_t kind, const sp_task* ops, const int64_t* counts,
+                        int32_t indent, char* buf, size_t* len);
+int sp_schedule_from_json(const char* text, sp_scenario* cfg_out, int32_t* kind_out, sp_task* ops,
+                          int64_t* counts, int32_t max_devices);
+int sp_report_to_json(const sp_scenario* cfg, int32_t kind, const int64_t* lengths, const sp_task* ops,
+                      const int64_t* counts, int32_t indent, int64_t memory_downsample, char* buf,
+                      size_t* len);
+
 /* ---- validate ---- */
 /* Violations as lines "code\tdevice\tdetail\n"; *n_violations set; *len in/out. */
 int sp_check_schedule(const sp_scenario* cfg, int32_t kind, const sp_task* ops, const int64_t* counts,
@@ -299,6 +314,11 @@ int sp_engine_step(sp_engine* eng, const int32_t* tokens, int32_t tokens_on_devi
                    sp_step_report* report);
 /* Executed op log of the last step for this engine (same layout as sp_schedule_ops). */
 int sp_engine_op_log(sp_engine* eng, sp_task* ops, int64_t* counts);
+/* The last step as a seqpipe.simreport.v1 document with MEASURED values (requires
+ * SP_FLAG_TIMELINE): task start/end in integer ns from the step start, per-device busy / idle /
+ * bubble ratios (sim.cpp:234-274 definitions), memory in bytes of activation records and
+ * KV-prefix slabs (+ at F end, - at B end). Text out via (buf, len) as sp_schedule_to_json. */
+int sp_engine_report_json(sp_engine* eng, int32_t indent, int64_t memory_downsample, char* buf, size_t* len);
 /* Per-op measured timeline of the last step (requires SP_FLAG_TIMELINE): start/end in ms. */
 int sp_engine_timeline(sp_engine* eng, double* start_ms, double* end_ms, int64_t* n);
 /* Parameter / gradient access in fp32. Names: "embed", "pos", "final_norm", "lm_head",

@@ -41,6 +41,11 @@ _SIGS = {
                                             P(C.c_size_t), P(C.c_int32)]),
     "ref_poq_run": (C.c_int, [P(C.c_int32), C.c_int32, P(C.c_int32), P(C.c_int32)]),
     "ref_time_planner": (C.c_int, [P(Scenario), C.c_int32, C.c_int32, C.c_int32, P(C.c_double)]),
+    "ref_schedule_to_json": (C.c_int, [P(Scenario), C.c_int32, P(Task), P(C.c_int64), C.c_int32, C.c_char_p,
+                                       P(C.c_size_t)]),
+    "ref_schedule_json_roundtrip": (C.c_int, [C.c_char_p, C.c_int32, C.c_char_p, P(C.c_size_t)]),
+    "ref_report_to_json": (C.c_int, [P(Scenario), C.c_int32, P(C.c_int64), P(Task), P(C.c_int64), C.c_int32,
+                                     C.c_int64, C.c_char_p, P(C.c_size_t)]),
 }
 _lib = None
 
@@ -208,3 +213,31 @@ def time_planner(cfg, kind="seq1f1b", mode="cwp", reps=20) -> float:
     out = C.c_double()
     _chk(lib().ref_time_planner(C.byref(s), pl.kind_id(kind), pl.PARTITION_MODES.index(mode), reps, C.byref(out)))
     return out.value
+
+
+def _text(fn, *args) -> str:
+    n = C.c_size_t(0)
+    _chk(fn(*args, None, C.byref(n)))
+    b = C.create_string_buffer(n.value)
+    _chk(fn(*args, b, C.byref(n)))
+    return b.value.decode()
+
+
+def schedule_to_json(schedule, indent: int = 2) -> str:
+    """Reference json_io.cpp:59-74 bytes of a schedule."""
+    s = schedule.config.to_c()
+    ops, counts = schedule.flat()
+    return _text(lib().ref_schedule_to_json, C.byref(s), pl.kind_id(schedule.kind), ops, counts, indent)
+
+
+def schedule_json_roundtrip(text: str, indent: int = 2) -> str:
+    """Reference dump(parse(text)) (json_io.cpp:59-97)."""
+    return _text(lib().ref_schedule_json_roundtrip, text.encode(), indent)
+
+
+def report_to_json(schedule, p, indent: int = 2, memory_downsample: int = 0) -> str:
+    """Reference json_io.cpp:99-159 bytes of simulate(schedule, p)."""
+    s = schedule.config.to_c()
+    ops, counts = schedule.flat()
+    return _text(lib().ref_report_to_json, C.byref(s), pl.kind_id(schedule.kind),
+                 (C.c_int64 * len(p.lengths))(*p.lengths), ops, counts, indent, memory_downsample)

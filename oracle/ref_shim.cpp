@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "seqpipe/cost.hpp"
+#include "seqpipe/json_io.hpp"
 #include "seqpipe/partition.hpp"
 #include "seqpipe/poq.hpp"
 #include "seqpipe/scenario.hpp"
@@ -325,6 +326,35 @@ int ref_time_planner(const sp_scenario* c, int32_t kind, int32_t mode, int32_t r
     }
     *best_ns = best;
   });
+}
+
+int ref_schedule_to_json(const sp_scenario* c, int32_t kind, const sp_task* ops, const int64_t* counts, int32_t indent,
+                         char* buf, size_t* len) {
+  try {
+    return text_out(schedule_to_json(sched_of(cfg_of(c), kind, ops, counts), indent), buf, len);
+  } catch (const std::exception& e) {
+    return fail(SP_ERR_RUNTIME, e.what());
+  }
+}
+
+// dump(parse(text)) through the reference: the canonical-form round trip.
+int ref_schedule_json_roundtrip(const char* text, int32_t indent, char* buf, size_t* len) {
+  try {
+    return text_out(schedule_to_json(schedule_from_json(text), indent), buf, len);
+  } catch (const std::exception& e) {
+    return fail(SP_ERR_INVALID_ARGUMENT, e.what());
+  }
+}
+
+int ref_report_to_json(const sp_scenario* c, int32_t kind, const int64_t* lengths, const sp_task* ops,
+                       const int64_t* counts, int32_t indent, int64_t downsample, char* buf, size_t* len) {
+  try {
+    auto cfg = cfg_of(c);
+    SimReport r = simulate(sched_of(cfg, kind, ops, counts), part_of(cfg, lengths));
+    return text_out(report_to_json(r, indent, static_cast<std::size_t>(downsample < 0 ? 0 : downsample)), buf, len);
+  } catch (const std::exception& e) {
+    return fail(SP_ERR_RUNTIME, e.what());
+  }
 }
 
 }  // extern "C"

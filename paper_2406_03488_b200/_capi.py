@@ -138,6 +138,7 @@ _SIGS = {
     "sp_engine_read_grad": (C.c_int, [C.c_void_p, C.c_char_p, P(C.c_float), C.c_int64]),
     "sp_engine_write_param": (C.c_int, [C.c_void_p, C.c_char_p, P(C.c_float), C.c_int64]),
     "sp_engine_memory": (C.c_int, [C.c_void_p, P(C.c_double), P(C.c_double)]),
+    "sp_engine_report_json": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_char_p, P(C.c_size_t)]),
     "sp_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
                           C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]),
     "sp_attention_fwd": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -145,6 +146,11 @@ _SIGS = {
     "sp_attention_bwd": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                    C.c_int32, C.c_int32, C.c_void_p]),
+    "sp_schedule_to_json": (C.c_int, [P(Scenario), C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_char_p,
+                                      P(C.c_size_t)]),
+    "sp_schedule_from_json": (C.c_int, [C.c_char_p, P(Scenario), P(C.c_int32), C.c_void_p, C.c_void_p, C.c_int32]),
+    "sp_report_to_json": (C.c_int, [P(Scenario), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
+                                    C.c_char_p, P(C.c_size_t)]),
     "sp_norm_fwd": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                               C.c_int64, C.c_int32, C.c_float, C.c_void_p]),
     "sp_norm_bwd": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -8,6 +8,7 @@
 #include "capi/capi_common.hpp"
 #include "engine/comm_plan.hpp"
 #include "engine/engine.hpp"
+#include "seqpipe/json_io.hpp"
 #include "seqpipe_b200.h"
 
 struct sp_engine {
@@ -175,6 +176,22 @@ int sp_engine_timeline(sp_engine* eng, double* start_ms, double* end_ms, int64_t
     std::copy(a.begin(), a.end(), start_ms);
     std::copy(b.begin(), b.end(), end_ms);
     *n = static_cast<int64_t>(a.size());
+  });
+}
+
+int sp_engine_report_json(sp_engine* eng, int32_t indent, int64_t memory_downsample, char* buf, size_t* len) {
+  return eguard([&] {
+    const std::string text = seqpipe::report_to_json(E(eng).measured_report(), indent,
+                                                     static_cast<std::size_t>(memory_downsample < 0 ? 0 : memory_downsample));
+    if (!len) throw std::invalid_argument("null length");
+    const size_t need = text.size() + 1;
+    if (!buf || *len < need) {
+      *len = need;
+      if (buf) throw std::length_error("buffer too small");
+      return;
+    }
+    std::memcpy(buf, text.c_str(), need);
+    *len = need;
   });
 }
 

@@ -9,6 +9,7 @@
 #include "seqpipe/partition.hpp"
 #include "seqpipe/scenario.hpp"
 #include "seqpipe/schedule.hpp"
+#include "seqpipe/json_io.hpp"
 #include "seqpipe/sim.hpp"
 #include "seqpipe/validate.hpp"
 #include "seqpipe_b200.h"
@@ -374,6 +375,47 @@ int sp_check_warmup_formulas(const sp_scenario* cfg, int32_t kind, const sp_task
     auto v = seqpipe::check_warmup_formulas(schedule_from_c(from_c(cfg), kind, ops, counts));
     if (n_violations) *n_violations = static_cast<int32_t>(v.size());
     return write_text(violations_text(v), buf, len);
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+
+int sp_schedule_to_json(const sp_scenario* cfg, int32_t kind, const sp_task* ops, const int64_t* counts, int32_t indent,
+                        char* buf, size_t* len) {
+  try {
+    const auto c = from_c(cfg);
+    return write_text(seqpipe::schedule_to_json(schedule_from_c(c, kind, ops, counts), indent), buf, len);
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int sp_schedule_from_json(const char* text, sp_scenario* cfg_out, int32_t* kind_out, sp_task* ops, int64_t* counts,
+                          int32_t max_devices) {
+  SP_GUARD({
+    if (!text || !cfg_out || !kind_out || !counts) throw std::invalid_argument("null argument");
+    const seqpipe::Schedule s = seqpipe::schedule_from_json(text);
+    if (static_cast<int32_t>(s.device_orders.size()) > max_devices)
+      throw std::out_of_range("schedule has more devices than max_devices");
+    to_c(s.config, cfg_out);
+    *kind_out = static_cast<int32_t>(s.kind);
+    std::size_t off = 0;
+    for (std::size_t d = 0; d < s.device_orders.size(); ++d) {
+      counts[d] = static_cast<int64_t>(s.device_orders[d].size());
+      if (ops)
+        for (const auto& t : s.device_orders[d]) ops[off++] = to_c(t);
+    }
+  });
+}
+
+int sp_report_to_json(const sp_scenario* cfg, int32_t kind, const int64_t* lengths, const sp_task* ops,
+                      const int64_t* counts, int32_t indent, int64_t memory_downsample, char* buf, size_t* len) {
+  try {
+    const auto c = from_c(cfg);
+    const auto rep = seqpipe::simulate(schedule_from_c(c, kind, ops, counts), partition_from_c(c, lengths, c.segments));
+    return write_text(seqpipe::report_to_json(rep, indent, static_cast<std::size_t>(memory_downsample < 0 ? 0 : memory_downsample)),
+                      buf, len);
   } catch (...) {
     return map_exception();
   }

@@ -13,6 +13,7 @@
 #include "engine/engine.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "engine/comm_plan.hpp"
@@ -321,6 +322,90 @@ std::vector<std::pair<Stage*, Param>> Engine::all_params() {
   for (auto& [v, st] : stages_)
     for (const Param& p : st->params()) out.emplace_back(st.get(), p);
   return out;
+}
+
+seqpipe::SimReport Engine::measured_report() const {
+  using seqpipe::Rational;
+  using seqpipe::TaskKind;
+  seqpipe::SimReport r;
+  r.kind = sched_.kind;
+  r.config = cfg_;
+  r.partition_lengths = len_;
+  const int P = cfg_.pipeline_size;
+  r.task_times.assign(static_cast<size_t>(P), {});
+  auto ns = [](double ms) { return static_cast<std::int64_t>(std::llround(ms * 1e6)); };
+  for (size_t i = 0; i < op_log_.size() && i < t_start_.size(); ++i) {
+    const seqpipe::Task& t = op_log_[i];
+    seqpipe::TaskTiming tt_i;
+    tt_i.task = t;
+    tt_i.start = Rational(ns(t_start_[i]));
+    tt_i.end = Rational(ns(t_end_[i]));
+    r.task_times[static_cast<size_t>(t.device - 1)].push_back(tt_i);
+  }
+  Rational makespan(0), sum_idle(0), sum_window(0), max_peak(0);
+  for (const auto& tt : r.task_times)
+    for (const auto& x : tt) makespan = std::max(makespan, x.end);
+  for (int d = 1; d <= P; ++d) {
+    auto& tt = r.task_times[static_cast<size_t>(d - 1)];
+    std::sort(tt.begin(), tt.end(), [](const auto& a, const auto& b) { return a.start < b.start; });
+    seqpipe::DeviceReport dev;
+    dev.device = d;
+    if (!tt.empty()) {
+      dev.first_start = tt.front().start;
+      dev.last_end = tt.front().end;
+      for (const auto& x : tt) {
+        dev.busy = dev.busy + (x.end - x.start);
+        dev.last_end = std::max(dev.last_end, x.end);
+      }
+      const Rational window = dev.last_end - dev.first_start;
+      dev.idle = window > Rational(0) ? window - dev.busy : Rational(0);
+      if (dev.idle < Rational(0)) dev.idle = Rational(0);  // overlapping events on one stream
+      dev.bubble_ratio = window > Rational(0) ? dev.idle / window : Rational(0);
+      dev.idle_in_makespan = makespan > dev.busy ? makespan - dev.busy : Rational(0);
+      dev.bubble_ratio_in_makespan = makespan > Rational(0) ? dev.idle_in_makespan / makespan : Rational(0);
+      sum_idle = sum_idle + dev.idle;
+      sum_window = sum_window + window;
+      // warm-up forwards: F tasks before the first backward (sim.cpp:240-250)
+      for (const auto& x : tt) {
+        if (x.task.kind != TaskKind::kForward) break;
+        ++dev.warmup_forward_tasks;
+      }
+      // memory series: + record (and the KV slab at segment 1) at F end, - at B end
+      std::vector<std::pair<Rational, std::int64_t>> ev;
+      for (const auto& x : tt) {
+        auto it = stages_.find(x.task.stage);
+        if (it == stages_.end()) continue;
+        const Stage& st = *it->second;
+        const std::int64_t b = st.record_bytes(x.task.segment) + (x.task.segment == 1 ? st.kv_slab_bytes() : 0);
+        if (x.task.kind == TaskKind::kForward) ev.push_back({x.end, b});
+        else if (x.task.kind == TaskKind::kFusedBackward) ev.push_back({x.end, -b});
+      }
+      std::stable_sort(ev.begin(), ev.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      std::int64_t live = 0, live_recs = 0, peak_recs = 0;
+      dev.memory_series.push_back({Rational(0), Rational(0)});
+      for (const auto& [t, b] : ev) {
+        live += b;
+        live_recs += b > 0 ? 1 : -1;
+        peak_recs = std::max(peak_recs, live_recs);
+        dev.memory_series.push_back({t, Rational(live)});
+        dev.peak_memory = std::max(dev.peak_memory, Rational(live));
+      }
+      dev.peak_allocations = peak_recs;
+    }
+    max_peak = std::max(max_peak, dev.peak_memory);
+    r.devices.push_back(std::move(dev));
+  }
+  r.makespan = makespan;
+  r.aggregate_bubble_ratio = sum_window > Rational(0) ? sum_idle / sum_window : Rational(0);
+  Rational in_mk(0);
+  for (const auto& dv : r.devices) in_mk = in_mk + dv.idle_in_makespan;
+  r.aggregate_bubble_ratio_in_makespan =
+      makespan > Rational(0) ? in_mk / (makespan * Rational(P)) : Rational(0);
+  r.max_peak_memory = max_peak;
+  r.modeled_throughput = makespan > Rational(0)
+                             ? Rational(static_cast<std::int64_t>(cfg_.micro_batches) * cfg_.seq_len) / makespan
+                             : Rational(0);
+  return r;
 }
 
 }  // namespace spe

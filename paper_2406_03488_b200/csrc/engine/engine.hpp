@@ -17,6 +17,7 @@
 #include "seqpipe/partition.hpp"
 #include "seqpipe/scenario.hpp"
 #include "seqpipe/schedule.hpp"
+#include "seqpipe/sim.hpp"
 #include "seqpipe_b200.h"
 
 namespace spe {
@@ -141,6 +142,10 @@ class Stage {
   double weight_bytes() const;
   double arena_bytes() const { return static_cast<double>(arena_.size()); }
   double live_peak_bytes() const { return static_cast<double>(arena_.live_peak); }
+  // Planned bytes of one (m, s) activation record (segment s, 1-based) and of a
+  // micro-batch's KV-prefix slab: the units of the measured memory series.
+  int64_t record_bytes(int s) const;
+  int64_t kv_slab_bytes() const;
   double dkv_bytes() const { return static_cast<double>(L_s_) * T_ * 2 * mc_.h * 4; }
   int stage() const { return stage_; }
   bool first() const { return stage_ == 1; }
@@ -201,6 +206,11 @@ class Engine {
   std::vector<std::vector<seqpipe::Task>> op_log_by_device() const;
   const std::vector<double>& t_start() const { return t_start_; }
   const std::vector<double>& t_end() const { return t_end_; }
+  // The last step as a SimReport (sim.hpp) with MEASURED values: integer
+  // nanoseconds from the step start, per-device busy / idle / bubble ratios with
+  // the definitions of sim.cpp:234-274, memory in bytes (activation records +
+  // KV-prefix slabs: +at F end, -at B end, sim.cpp:276-311).
+  seqpipe::SimReport measured_report() const;
   Stage* stage_for_param(const std::string& name, Param* out);
   std::vector<std::pair<Stage*, Param>> all_params();
   int device() const { return dev_; }

@@ -268,6 +268,9 @@ DualArena plan_stage_memory(const ModelCfg& mc, const seqpipe::ScenarioConfig& c
   return replay_plan(mc, cfg, len, order, stage, seg, kvo);
 }
 
+int64_t Stage::record_bytes(int s) const { return seg_bytes(mc_, L_s_, len_[static_cast<size_t>(s - 1)], esz_); }
+int64_t Stage::kv_slab_bytes() const { return static_cast<int64_t>(L_s_) * T_ * 2 * mc_.h * static_cast<int64_t>(esz_); }
+
 void Stage::plan_arena(const std::vector<seqpipe::Task>& order) {
   arena_ = replay_plan(mc_, cfg_, len_, order, stage_, seg_off_, kv_off_);
   if (arena_ptr_) cudaFree(arena_ptr_);

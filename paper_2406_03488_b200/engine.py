@@ -105,6 +105,14 @@ class Engine:
         _check(_capi.lib().sp_engine_step(self._h, ptr, 1 if on_device else 0, C.byref(rep)))
         return rep
 
+    def report_json(self, indent: int = 2, memory_downsample: int = 0) -> str:
+        """The last step as seqpipe.simreport.v1 with measured ns times (needs FLAG_TIMELINE)."""
+        n = C.c_size_t(0)
+        _check(_capi.lib().sp_engine_report_json(self._h, indent, memory_downsample, None, C.byref(n)))
+        b = C.create_string_buffer(n.value)
+        _check(_capi.lib().sp_engine_report_json(self._h, indent, memory_downsample, b, C.byref(n)))
+        return b.value.decode()
+
     def op_log(self) -> pl.Schedule:
         P = self.cfg.pipeline_size
         counts = (C.c_int64 * P)()

@@ -511,3 +511,42 @@ def check_warmup_formulas(schedule: Schedule):
 
 def violations_to_string(vs) -> str:
     return "".join(f"{v.code}{f' [device {v.device}]' if v.device > 0 else ''}: {v.detail}\n" for v in vs)
+
+
+# ---------------------------------------------------------------- JSON wire formats
+# seqpipe.schedule.v1 / seqpipe.simreport.v1 (reference core/include/seqpipe/json_io.hpp:19-26).
+
+def _text_out(fn, *args) -> str:
+    n = C.c_size_t(0)
+    _check(fn(*args, None, C.byref(n)))
+    b = C.create_string_buffer(n.value)
+    _check(fn(*args, b, C.byref(n)))
+    return b.value.decode()
+
+
+def schedule_to_json(schedule: Schedule, indent: int = 2) -> str:
+    c = schedule.config.to_c()
+    ops, counts = schedule.flat()
+    return _text_out(_capi.lib().sp_schedule_to_json, C.byref(c), kind_id(schedule.kind), ops, counts, indent)
+
+
+def schedule_from_json(text: str, max_devices: int = 4096) -> Schedule:
+    c = _capi.Scenario()
+    kind = C.c_int32(0)
+    counts = (C.c_int64 * max_devices)()
+    raw = text.encode()
+    _check(_capi.lib().sp_schedule_from_json(raw, C.byref(c), C.byref(kind), None, counts, max_devices))
+    cfg = ScenarioConfig.from_c(c)
+    total = sum(counts[: cfg.pipeline_size])
+    ops = (_T * max(1, total))()
+    _check(_capi.lib().sp_schedule_from_json(raw, C.byref(c), C.byref(kind), ops, counts, max_devices))
+    return Schedule(cfg, SCHEDULE_KINDS[kind.value], _unflatten(cfg.pipeline_size, ops, counts))
+
+
+def report_to_json(schedule: Schedule, partition: SequencePartition, indent: int = 2,
+                   memory_downsample: int = 0) -> str:
+    """simulate(schedule, partition) serialised as seqpipe.simreport.v1."""
+    c = schedule.config.to_c()
+    ops, counts = schedule.flat()
+    return _text_out(_capi.lib().sp_report_to_json, C.byref(c), kind_id(schedule.kind), _lengths(partition), ops,
+                     counts, indent, memory_downsample)

@@ -148,3 +148,35 @@ def test_optimizer_step_changes_weights(gpu):
     for _ in range(3):
         l2 = eng.step(tok).loss
     assert l2 < l1
+
+
+def test_measured_report_and_executed_schedule_json(gpu):
+    """(f3) wire formats on the engine: the executed op log as seqpipe.schedule.v1 (read back
+    by the compiled reference, byte-identical to the planned schedule's document) and the
+    measured step as seqpipe.simreport.v1 (ns times, sim.cpp metric definitions)."""
+    import json
+
+    model = tiny_model(layers=4, hidden=128, heads=2, ffn=256, vocab=256, max_seq=512)
+    model.flags = E.FLAG_TIMELINE
+    cfg = scenario(model, P=4, M=6, k=4, T=512)
+    eng, part, tok, rep = run(model, cfg)
+    log = eng.op_log()
+    text = pl.schedule_to_json(log)
+    assert text == pl.schedule_to_json(ref.generate(cfg, "seq1f1b", part))
+    assert ref.schedule_json_roundtrip(text) == text
+    doc = json.loads(eng.report_json())
+    assert doc["schema"] == "seqpipe.simreport.v1" and doc["kind"] == "seq1f1b"
+    assert doc["partition"] == part.lengths
+    modeled = json.loads(ref.report_to_json(ref.generate(cfg, "seq1f1b", part), part))
+    for dev, mod in zip(doc["devices"], modeled["devices"]):
+        tasks = dev["tasks"]
+        assert [(t["kind"], t["m"], t["s"]) for t in tasks] == [(t["kind"], t["m"], t["s"]) for t in mod["tasks"]]
+        assert all(int(t["end"]) >= int(t["start"]) >= 0 for t in tasks)
+        first, last, busy = int(dev["first_start"]), int(dev["last_end"]), int(dev["busy"])
+        assert busy <= last - first + len(tasks)  # ns rounding per task
+        num, _, den = dev["bubble_ratio"].partition("/")
+        assert 0 <= int(num) / int(den or 1) <= 1
+        assert dev["warmup_forward_tasks"] == mod["warmup_forward_tasks"]
+        assert dev["peak_allocations"] == mod["peak_allocations"]
+        assert int(dev["peak_memory"].split("/")[0]) > 0
+    eng.close()
