@@ -152,8 +152,13 @@ void Engine::exec_op(const seqpipe::Task& t, int i, int pos) {
   Stage* st = stage_obj(t.stage);
   Stage::Seg& sg = st->seg(t.micro_batch, t.segment);
   const bool fwd = t.kind == seqpipe::TaskKind::kForward;
-  if (t.kind != seqpipe::TaskKind::kForward && t.kind != seqpipe::TaskKind::kFusedBackward)
-    throw std::invalid_argument("engine executes F and B tasks only");
+  if (t.kind == seqpipe::TaskKind::kWeightGrad) {  // zero-bubble W: local weight-gradient GEMMs, no transfers
+    SPK_CUDA(cudaEventRecord(ev_start_[i], s_));
+    st->backward_weight(t.micro_batch, t.segment);
+    SPK_CUDA(cudaEventRecord(ev_end_[i], s_));
+    return;
+  }
+  const bool input_only = t.kind == seqpipe::TaskKind::kInputGrad;  // zero-bubble I: B without the W GEMMs
   const std::vector<sp_comm_op>* pre = nullptr;
   const std::vector<sp_comm_op>* post = nullptr;
   if (world_ > 1) {
@@ -193,7 +198,10 @@ void Engine::exec_op(const seqpipe::Task& t, int i, int pos) {
     dx_target = stage_obj(t.stage - 1)->seg(t.micro_batch, t.segment).dy_in;  // in-process hand-off
   }
   SPK_CUDA(cudaEventRecord(ev_start_[i], s_));
-  st->backward(t.micro_batch, t.segment, dx_target, tokens_dev_);
+  if (input_only)
+    st->backward_input(t.micro_batch, t.segment, dx_target, tokens_dev_);
+  else
+    st->backward(t.micro_batch, t.segment, dx_target, tokens_dev_);
   SPK_CUDA(cudaEventRecord(ev_end_[i], s_));
   if (slot >= 0) {
     for (const sp_comm_op& c : *post) {
@@ -378,7 +386,8 @@ seqpipe::SimReport Engine::measured_report() const {
         const Stage& st = *it->second;
         const std::int64_t b = st.record_bytes(x.task.segment) + (x.task.segment == 1 ? st.kv_slab_bytes() : 0);
         if (x.task.kind == TaskKind::kForward) ev.push_back({x.end, b});
-        else if (x.task.kind == TaskKind::kFusedBackward) ev.push_back({x.end, -b});
+        else if (x.task.kind == TaskKind::kFusedBackward || x.task.kind == TaskKind::kWeightGrad)
+          ev.push_back({x.end, -b});  // zero-bubble kinds free at W end (sim.cpp:279-293)
       }
       std::stable_sort(ev.begin(), ev.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
       std::int64_t live = 0, live_recs = 0, peak_recs = 0;

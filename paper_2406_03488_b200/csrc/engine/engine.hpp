@@ -117,6 +117,10 @@ class Stage {
     void* dy_in = nullptr;    // gradient w.r.t. the stage output [n,h]
     std::vector<void*> q, o, x_mid, u;
     std::vector<float*> mean1, rstd1, mean2, rstd2, lse;
+    // Zero-bubble split (I / W tasks): weight-gradient operands the I task leaves
+    // for the W task, per layer: layer-output grad [n,h], activation grad
+    // [n,Fup], attention-output grad [n,h], dQKV [n,3h].
+    std::vector<void*> w_dy, w_du, w_dxm, w_dqkv;
   };
 
   void plan_arena(const std::vector<seqpipe::Task>& order);
@@ -125,6 +129,11 @@ class Stage {
   void forward(int m, int s, const int32_t* tokens_dev, double* loss_acc, float loss_scale);
   // dx_target: where the gradient w.r.t. this stage's input goes (another stage's dy_in or a send buffer).
   void backward(int m, int s, void* dx_target, const int32_t* tokens_dev);
+  // Zero-bubble split (reference TaskKind I / W, schedule.cpp:217-309): I = the
+  // backward without the weight-gradient GEMMs (their operands saved in the W
+  // record), W = those GEMMs (norm-output / activation operands recomputed).
+  void backward_input(int m, int s, void* dx_target, const int32_t* tokens_dev);
+  void backward_weight(int m, int s);
 
   Seg& seg(int m, int s) { return segs_[(m - 1) * k_ + (s - 1)]; }
   void* kv(int m, int layer) const;  // [T, 2h] slab of layer (local index)
@@ -184,7 +193,8 @@ class Stage {
 
   DualArena arena_;
   uint8_t* arena_ptr_ = nullptr;
-  std::vector<int64_t> seg_off_, kv_off_;
+  std::vector<int64_t> seg_off_, kv_off_, w_off_;
+  void backward_impl(int m, int s, void* dx_target, const int32_t* tokens_dev, bool defer_w);
   std::vector<Seg> segs_;
   float* dkv_ = nullptr;
 

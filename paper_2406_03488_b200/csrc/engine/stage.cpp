@@ -233,46 +233,67 @@ static int64_t seg_bytes(const ModelCfg& mc, int L_s, int64_t n, size_t esz) {
   return b + 256LL * (8 * L_s + 4);        // per-field alignment slack
 }
 
+// Bytes of one (m, s) zero-bubble W record (operands of the deferred
+// weight-gradient GEMMs): per layer dy [n,h], du [n,Fup], dxm [n,h], dqkv [n,3h].
+static int64_t w_bytes(const ModelCfg& mc, int L_s, int64_t n, size_t esz) {
+  return static_cast<int64_t>(L_s) * n * (5LL * mc.h + mc.Fup) * static_cast<int64_t>(esz) + 256LL * 4 * L_s;
+}
+
 // Host-only replay of the arena plan of one stage (no device memory): the
-// analytical activation footprint used to report OOM configurations.
+// analytical activation footprint used to report OOM configurations. F
+// allocates the (m,s) record (and at s = 1 the micro-batch's KV slab); B frees
+// them; with the zero-bubble split I allocates the W record and W frees all
+// three, as the reference frees memory at W end (sim.cpp:279-293).
 static DualArena replay_plan(const ModelCfg& mc, const seqpipe::ScenarioConfig& cfg, const std::vector<int64_t>& len,
                              const std::vector<seqpipe::Task>& order, int stage, std::vector<int64_t>& seg,
-                             std::vector<int64_t>& kvo) {
+                             std::vector<int64_t>& kvo, std::vector<int64_t>& wo) {
   const int L_s = mc.L / cfg.total_stages();
   const size_t esz = spk::dtype_size(mc.dt);
   const int64_t kv_bytes = static_cast<int64_t>(L_s) * cfg.seq_len * 2 * mc.h * esz;
   DualArena a;
   seg.assign(static_cast<size_t>(cfg.micro_batches) * cfg.segments, -1);
+  wo.assign(static_cast<size_t>(cfg.micro_batches) * cfg.segments, -1);
   kvo.assign(static_cast<size_t>(cfg.micro_batches), -1);
   for (const seqpipe::Task& t : order) {
     if (t.stage != stage) continue;
     const size_t idx = static_cast<size_t>(t.micro_batch - 1) * cfg.segments + (t.segment - 1);
-    if (t.kind == seqpipe::TaskKind::kForward) {
-      if (t.segment == 1) kvo[t.micro_batch - 1] = a.alloc(0, kv_bytes);
-      seg[idx] = a.alloc(1, seg_bytes(mc, L_s, len[t.segment - 1], esz));
-    } else if (t.kind == seqpipe::TaskKind::kFusedBackward) {
-      a.release(1, seg[idx]);
-      if (t.segment == 1) a.release(0, kvo[t.micro_batch - 1]);
-    } else {
-      throw std::invalid_argument("engine executes F and B tasks (zero-bubble I/W split not supported yet)");
+    switch (t.kind) {
+      case seqpipe::TaskKind::kForward:
+        if (t.segment == 1) kvo[t.micro_batch - 1] = a.alloc(0, kv_bytes);
+        seg[idx] = a.alloc(1, seg_bytes(mc, L_s, len[t.segment - 1], esz));
+        break;
+      case seqpipe::TaskKind::kFusedBackward:
+        a.release(1, seg[idx]);
+        if (t.segment == 1) a.release(0, kvo[t.micro_batch - 1]);
+        break;
+      case seqpipe::TaskKind::kInputGrad:
+        wo[idx] = a.alloc(1, w_bytes(mc, L_s, len[t.segment - 1], esz));
+        break;
+      case seqpipe::TaskKind::kWeightGrad:
+        a.release(1, wo[idx]);
+        a.release(1, seg[idx]);
+        if (t.segment == 1) a.release(0, kvo[t.micro_batch - 1]);
+        break;
     }
   }
   for (int64_t& o : seg)
     if (o >= 0) o += a.pool[0].size;  // record pool sits after the slab pool
+  for (int64_t& o : wo)
+    if (o >= 0) o += a.pool[0].size;
   return a;
 }
 
 DualArena plan_stage_memory(const ModelCfg& mc, const seqpipe::ScenarioConfig& cfg, const std::vector<int64_t>& len,
                             const std::vector<seqpipe::Task>& order, int stage) {
-  std::vector<int64_t> seg, kvo;
-  return replay_plan(mc, cfg, len, order, stage, seg, kvo);
+  std::vector<int64_t> seg, kvo, wo;
+  return replay_plan(mc, cfg, len, order, stage, seg, kvo, wo);
 }
 
 int64_t Stage::record_bytes(int s) const { return seg_bytes(mc_, L_s_, len_[static_cast<size_t>(s - 1)], esz_); }
 int64_t Stage::kv_slab_bytes() const { return static_cast<int64_t>(L_s_) * T_ * 2 * mc_.h * static_cast<int64_t>(esz_); }
 
 void Stage::plan_arena(const std::vector<seqpipe::Task>& order) {
-  arena_ = replay_plan(mc_, cfg_, len_, order, stage_, seg_off_, kv_off_);
+  arena_ = replay_plan(mc_, cfg_, len_, order, stage_, seg_off_, kv_off_, w_off_);
   if (arena_ptr_) cudaFree(arena_ptr_);
   SPK_CUDA(cudaMalloc(&arena_ptr_, std::max<int64_t>(arena_.size(), 256)));
   bind_step();
@@ -317,6 +338,19 @@ void Stage::bind_step() {
         g.mean2[l] = static_cast<float*>(take(n * 4));
         g.rstd2[l] = static_cast<float*>(take(n * 4));
         g.lse[l] = static_cast<float*>(take(n * mc_.H * 4));
+      }
+      g.w_dy.assign(static_cast<size_t>(L_s_), nullptr);
+      g.w_du.assign(static_cast<size_t>(L_s_), nullptr);
+      g.w_dxm.assign(static_cast<size_t>(L_s_), nullptr);
+      g.w_dqkv.assign(static_cast<size_t>(L_s_), nullptr);
+      if (w_off_.size() > idx && w_off_[idx] >= 0) {
+        p = arena_ptr_ + w_off_[idx];
+        for (int l = 0; l < L_s_; ++l) {
+          g.w_dy[l] = take(n * h * esz_);
+          g.w_du[l] = take(n * mc_.Fup * esz_);
+          g.w_dxm[l] = take(n * h * esz_);
+          g.w_dqkv[l] = take(n * 3 * h * esz_);
+        }
       }
     }
   }
@@ -478,6 +512,42 @@ void Stage::head_forward_backward(Seg& sg, int m, const int32_t* tokens, double*
 }
 
 void Stage::backward(int m, int s, void* dx_target, const int32_t* tokens) {
+  backward_impl(m, s, dx_target, tokens, false);
+}
+
+void Stage::backward_input(int m, int s, void* dx_target, const int32_t* tokens) {
+  backward_impl(m, s, dx_target, tokens, true);
+}
+
+// W task: the four weight-gradient GEMMs per layer from the operands the I task
+// saved; the norm outputs and the activation output are recomputed (elementwise).
+void Stage::backward_weight(int m, int s) {
+  Seg& sg = seg(m, s);
+  const int64_t n = sg.n, h = mc_.h, F = mc_.F, Fu = mc_.Fup;
+  const DType dt = mc_.dt;
+  if (sg.w_dy.empty() || !sg.w_dy[0]) throw std::logic_error("W task without a planned W record");
+  for (int l = L_s_ - 1; l >= 0; --l) {
+    const LayerW& w = lw_[l];
+    spk::act_fwd(dt, mc_.family, sg.u[l], w_big1_, n, F, s_);
+    GemmArgs g = G(dt, h, F, n, sg.w_dy[l], h, false, w_big1_, F, false, wg(w.w2), F, DType::kF32);
+    g.epi = Epi::kAccumF32;
+    gemm(g, 2.0 * n * h * F);
+    spk::norm_apply(dt, mc_.rms(), sg.x_mid[l], wm(w.norm2), sg.mean2[l], sg.rstd2[l], w_a_, n, mc_.h, s_);
+    g = G(dt, Fu, h, n, sg.w_du[l], Fu, false, w_a_, h, false, wg(w.w1), h, DType::kF32);
+    g.epi = Epi::kAccumF32;
+    gemm(g, 2.0 * n * Fu * h);
+    g = G(dt, h, h, n, sg.w_dxm[l], h, false, sg.o[l], h, false, wg(w.wo), h, DType::kF32);
+    g.epi = Epi::kAccumF32;
+    gemm(g, 2.0 * n * h * h);
+    spk::norm_apply(dt, mc_.rms(), sg.x_in[l], wm(w.norm1), sg.mean1[l], sg.rstd1[l], w_a_, n, mc_.h, s_);
+    g = G(dt, 3 * h, h, n, sg.w_dqkv[l], 3 * h, false, w_a_, h, false, wg(w.wqkv), h, DType::kF32);
+    g.epi = Epi::kAccumF32;
+    gemm(g, 2.0 * n * 3 * h * h);
+    launches += 2;
+  }
+}
+
+void Stage::backward_impl(int m, int s, void* dx_target, const int32_t* tokens, bool defer_w) {
   Seg& sg = seg(m, s);
   const int64_t n = sg.n, pos0 = sg.pos0, h = mc_.h, F = mc_.F, Fu = mc_.Fup;
   const DType dt = mc_.dt;
@@ -487,23 +557,38 @@ void Stage::backward(int m, int s, void* dx_target, const int32_t* tokens) {
   for (int l = L_s_ - 1; l >= 0; --l) {
     const LayerW& w = lw_[l];
     // ---- MLP: y = x_mid + act(norm2(x_mid) W1^T) W2^T
-    spk::norm_apply(dt, mc_.rms(), sg.x_mid[l], wm(w.norm2), sg.mean2[l], sg.rstd2[l], w_a_, n, mc_.h, s_);
-    spk::act_fwd(dt, mc_.family, sg.u[l], w_big1_, n, F, s_);
-    GemmArgs g = G(dt, h, F, n, dy, h, false, w_big1_, F, false, wg(w.w2), F, DType::kF32);
-    g.epi = Epi::kAccumF32;
-    gemm(g, 2.0 * n * h * F);
+    if (!defer_w) {  // recomputed operands of the W2 / W1 weight gradients
+      spk::norm_apply(dt, mc_.rms(), sg.x_mid[l], wm(w.norm2), sg.mean2[l], sg.rstd2[l], w_a_, n, mc_.h, s_);
+      spk::act_fwd(dt, mc_.family, sg.u[l], w_big1_, n, F, s_);
+    }
+    GemmArgs g;
+    if (defer_w) {
+      SPK_CUDA(cudaMemcpyAsync(sg.w_dy[l], dy, esz_ * n * h, cudaMemcpyDeviceToDevice, s_));
+    } else {
+      g = G(dt, h, F, n, dy, h, false, w_big1_, F, false, wg(w.w2), F, DType::kF32);
+      g.epi = Epi::kAccumF32;
+      gemm(g, 2.0 * n * h * F);
+    }
     gemm(G(dt, n, F, h, dy, h, true, wc(w.w2), F, false, w_big2_, F, dt), 2.0 * n * h * F);
     spk::act_bwd(dt, mc_.family, sg.u[l], w_big2_, w_big1_, n, F, s_);
-    g = G(dt, Fu, h, n, w_big1_, Fu, false, w_a_, h, false, wg(w.w1), h, DType::kF32);
-    g.epi = Epi::kAccumF32;
-    gemm(g, 2.0 * n * Fu * h);
+    if (defer_w) {
+      SPK_CUDA(cudaMemcpyAsync(sg.w_du[l], w_big1_, esz_ * n * Fu, cudaMemcpyDeviceToDevice, s_));
+    } else {
+      g = G(dt, Fu, h, n, w_big1_, Fu, false, w_a_, h, false, wg(w.w1), h, DType::kF32);
+      g.epi = Epi::kAccumF32;
+      gemm(g, 2.0 * n * Fu * h);
+    }
     gemm(G(dt, n, h, Fu, w_big1_, Fu, true, wc(w.w1), h, false, w_t1_, h, dt), 2.0 * n * Fu * h);
     spk::norm_bwd(dt, mc_.rms(), w_t1_, sg.x_mid[l], wm(w.norm2), sg.mean2[l], sg.rstd2[l], dy, w_t2_, wg(w.norm2), n,
                   mc_.h, s_);
     // ---- attention: x_mid = x + attn(norm1(x)) Wo^T
-    g = G(dt, h, h, n, w_t2_, h, false, sg.o[l], h, false, wg(w.wo), h, DType::kF32);
-    g.epi = Epi::kAccumF32;
-    gemm(g, 2.0 * n * h * h);
+    if (defer_w) {
+      SPK_CUDA(cudaMemcpyAsync(sg.w_dxm[l], w_t2_, esz_ * n * h, cudaMemcpyDeviceToDevice, s_));
+    } else {
+      g = G(dt, h, h, n, w_t2_, h, false, sg.o[l], h, false, wg(w.wo), h, DType::kF32);
+      g.epi = Epi::kAccumF32;
+      gemm(g, 2.0 * n * h * h);
+    }
     gemm(G(dt, n, h, h, w_t2_, h, true, wc(w.wo), h, false, w_t3_, h, dt), 2.0 * n * h * h);
     float* dkv_l = dkv(l);
     // Algorithmic count: backward = 2x forward attention FLOPs (SURVEY §8d convention).
@@ -520,10 +605,14 @@ void Stage::backward(int m, int s, void* dx_target, const int32_t* tokens) {
       launches += 2;
     }
     spk::assemble_dqkv(dt, w_t1_, dkv_rows, w_dqkv_, n, mc_.h, s_);
-    spk::norm_apply(dt, mc_.rms(), sg.x_in[l], wm(w.norm1), sg.mean1[l], sg.rstd1[l], w_a_, n, mc_.h, s_);
-    g = G(dt, 3 * h, h, n, w_dqkv_, 3 * h, false, w_a_, h, false, wg(w.wqkv), h, DType::kF32);
-    g.epi = Epi::kAccumF32;
-    gemm(g, 2.0 * n * 3 * h * h);
+    if (defer_w) {
+      SPK_CUDA(cudaMemcpyAsync(sg.w_dqkv[l], w_dqkv_, esz_ * n * 3 * h, cudaMemcpyDeviceToDevice, s_));
+    } else {
+      spk::norm_apply(dt, mc_.rms(), sg.x_in[l], wm(w.norm1), sg.mean1[l], sg.rstd1[l], w_a_, n, mc_.h, s_);
+      g = G(dt, 3 * h, h, n, w_dqkv_, 3 * h, false, w_a_, h, false, wg(w.wqkv), h, DType::kF32);
+      g.epi = Epi::kAccumF32;
+      gemm(g, 2.0 * n * 3 * h * h);
+    }
     gemm(G(dt, n, h, 3 * h, w_dqkv_, 3 * h, true, wc(w.wqkv), h, false, w_t1_, h, dt), 2.0 * n * 3 * h * h);
     void* dx = (l > 0) ? w_t2_ : (first() ? w_t3_ : dx_target);
     spk::norm_bwd(dt, mc_.rms(), w_t1_, sg.x_in[l], wm(w.norm1), sg.mean1[l], sg.rstd1[l], w_t2_, dx, wg(w.norm1), n,

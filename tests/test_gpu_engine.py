@@ -180,3 +180,22 @@ def test_measured_report_and_executed_schedule_json(gpu):
         assert dev["peak_allocations"] == mod["peak_allocations"]
         assert int(dev["peak_memory"].split("/")[0]) > 0
     eng.close()
+
+
+@pytest.mark.parametrize("kind,k,dtype,tol", [("zb1p", 1, E.F32, TOL_F32), ("seqzb1p", 4, E.F32, TOL_F32),
+                                              ("seqzb1p", 4, E.BF16, TOL_BF16)])
+def test_zero_bubble_input_weight_split(gpu, kind, k, dtype, tol):
+    """(f2) SeqZB1P / ZB1P: the engine executes the reference's I / W op tables
+    (schedule.cpp:217-309, W placed in idle gaps by simulate()) -- I = backward without
+    the weight-gradient GEMMs, W = those GEMMs from the operands I saved -- and the step
+    matches the CPU oracle; the executed log is the reference's and passes its checker."""
+    model = tiny_model(dtype=dtype, layers=4, hidden=128, heads=2, ffn=256, vocab=256, max_seq=512)
+    cfg = scenario(model, P=2, M=3, k=k, T=512)
+    eng, part, tok, rep = run(model, cfg, kind=kind, mode="cwp" if k > 1 else "even")
+    log = eng.op_log()
+    assert log.device_orders == ref.generate(cfg, kind, part).device_orders
+    assert ref.check_schedule(log) == []
+    assert sum(1 for o in log.device_orders for t in o if t.kind == "W") == cfg.micro_batches * k * cfg.pipeline_size
+    compare(eng, model, part, tok, rep, tol)
+    eng.close()
+
