@@ -69,6 +69,27 @@ struct MissingDependencyError : std::runtime_error {
 
 SimReport simulate(const Schedule& schedule, const SequencePartition& partition);
 
+// Side-by-side comparison of >= 2 reports (reference sim.hpp:82-99,
+// sim.cpp:319-367). Reports must share seq_len and micro_batches unless
+// allow_mixed; throws std::invalid_argument otherwise or for < 2 reports.
+struct ComparisonRow {
+  std::string kind;
+  ScenarioConfig config;
+  Rational makespan{0};
+  Rational bubble_ratio{0};
+  Rational max_peak_memory{0};
+  Rational throughput{0};
+};
+
+struct ComparisonTable {
+  std::vector<ComparisonRow> rows;
+  // CSV: config columns, the four metrics (6 decimals) and their ratios to the
+  // first row (empty where the first row's value is zero).
+  std::string to_csv() const;
+};
+
+ComparisonTable compare(const std::vector<SimReport>& reports, bool allow_mixed = false);
+
 // Position-level replay order: a topological interleaving of all device
 // orders (device-round-robin, each device advancing while its front task is
 // ready). The single-GPU engine executes ops in exactly this order.

@@ -198,6 +198,20 @@ int sp_report_to_json(const sp_scenario* cfg, int32_t kind, const int64_t* lengt
                       const int64_t* counts, int32_t indent, int64_t memory_downsample, char* buf,
                       size_t* len);
 
+/* ---- Timeline rendering and comparison (core/include/seqpipe/render.hpp:15-21, core/src/render.cpp:46-124;
+ * core/include/seqpipe/sim.hpp:82-99, core/src/sim.cpp:319-367) ----
+ * sp_render_gantt: simulate(schedule, partition) drawn as text (SP_RENDER_ASCII, `width` cells per row)
+ * or SVG (SP_RENDER_SVG); sp_engine_render_gantt draws the engine's last MEASURED step (ns times,
+ * needs SP_FLAG_TIMELINE). sp_compare_csv: compare() of the simulations of n >= 2 op tables, as CSV
+ * (ComparisonTable::to_csv); reports must share seq_len / micro_batches unless allow_mixed.
+ * Text out via (buf, len) as above. */
+enum { SP_RENDER_ASCII = 0, SP_RENDER_SVG = 1 };
+int sp_render_gantt(const sp_scenario* cfg, int32_t kind, const int64_t* lengths, const sp_task* ops,
+                    const int64_t* counts, int32_t format, int32_t width, char* buf, size_t* len);
+int sp_compare_csv(int32_t n, const sp_scenario* cfgs, const int32_t* kinds, const int64_t* const* lengths,
+                   const sp_task* const* ops, const int64_t* const* counts, int32_t allow_mixed, char* buf,
+                   size_t* len);
+
 /* ---- validate ---- */
 /* Violations as lines "code\tdevice\tdetail\n"; *n_violations set; *len in/out. */
 int sp_check_schedule(const sp_scenario* cfg, int32_t kind, const sp_task* ops, const int64_t* counts,
@@ -319,6 +333,7 @@ int sp_engine_op_log(sp_engine* eng, sp_task* ops, int64_t* counts);
  * bubble ratios (sim.cpp:234-274 definitions), memory in bytes of activation records and
  * KV-prefix slabs (+ at F end, - at B end). Text out via (buf, len) as sp_schedule_to_json. */
 int sp_engine_report_json(sp_engine* eng, int32_t indent, int64_t memory_downsample, char* buf, size_t* len);
+int sp_engine_render_gantt(sp_engine* eng, int32_t format, int32_t width, char* buf, size_t* len);
 /* Per-op measured timeline of the last step (requires SP_FLAG_TIMELINE): start/end in ms. */
 int sp_engine_timeline(sp_engine* eng, double* start_ms, double* end_ms, int64_t* n);
 /* Parameter / gradient access in fp32. Names: "embed", "pos", "final_norm", "lm_head",

@@ -46,6 +46,10 @@ _SIGS = {
     "ref_schedule_json_roundtrip": (C.c_int, [C.c_char_p, C.c_int32, C.c_char_p, P(C.c_size_t)]),
     "ref_report_to_json": (C.c_int, [P(Scenario), C.c_int32, P(C.c_int64), P(Task), P(C.c_int64), C.c_int32,
                                      C.c_int64, C.c_char_p, P(C.c_size_t)]),
+    "ref_render_gantt": (C.c_int, [P(Scenario), C.c_int32, P(C.c_int64), P(Task), P(C.c_int64), C.c_int32,
+                                   C.c_int32, C.c_char_p, P(C.c_size_t)]),
+    "ref_compare_csv": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                  C.c_char_p, P(C.c_size_t)]),
 }
 _lib = None
 
@@ -241,3 +245,17 @@ def report_to_json(schedule, p, indent: int = 2, memory_downsample: int = 0) -> 
     ops, counts = schedule.flat()
     return _text(lib().ref_report_to_json, C.byref(s), pl.kind_id(schedule.kind),
                  (C.c_int64 * len(p.lengths))(*p.lengths), ops, counts, indent, memory_downsample)
+
+
+def render_gantt(schedule, p, fmt: str = "ascii", width: int = 120) -> str:
+    """Reference render.cpp:46-124 bytes of simulate(schedule, p)."""
+    s = schedule.config.to_c()
+    ops, counts = schedule.flat()
+    return _text(lib().ref_render_gantt, C.byref(s), pl.kind_id(schedule.kind),
+                 (C.c_int64 * len(p.lengths))(*p.lengths), ops, counts, pl.RENDER_FORMATS[fmt], width)
+
+
+def compare_csv(runs, allow_mixed: bool = False) -> str:
+    """Reference sim.cpp:319-367: compare(simulate(...) for each run).to_csv()."""
+    n, cfgs, kinds, lens, opss, cnts, _keep = pl._compare_args(runs)
+    return _text(lib().ref_compare_csv, n, cfgs, kinds, lens, opss, cnts, int(allow_mixed))

@@ -14,6 +14,7 @@
 
 #include "seqpipe/cost.hpp"
 #include "seqpipe/json_io.hpp"
+#include "seqpipe/render.hpp"
 #include "seqpipe/partition.hpp"
 #include "seqpipe/poq.hpp"
 #include "seqpipe/scenario.hpp"
@@ -352,6 +353,34 @@ int ref_report_to_json(const sp_scenario* c, int32_t kind, const int64_t* length
     auto cfg = cfg_of(c);
     SimReport r = simulate(sched_of(cfg, kind, ops, counts), part_of(cfg, lengths));
     return text_out(report_to_json(r, indent, static_cast<std::size_t>(downsample < 0 ? 0 : downsample)), buf, len);
+  } catch (const std::exception& e) {
+    return fail(SP_ERR_RUNTIME, e.what());
+  }
+}
+
+int ref_render_gantt(const sp_scenario* c, int32_t kind, const int64_t* lengths, const sp_task* ops,
+                     const int64_t* counts, int32_t format, int32_t width, char* buf, size_t* len) {
+  try {
+    auto cfg = cfg_of(c);
+    SimReport r = simulate(sched_of(cfg, kind, ops, counts), part_of(cfg, lengths));
+    return text_out(format == 1 ? render_svg_gantt(r) : render_ascii_gantt(r, width), buf, len);
+  } catch (const std::exception& e) {
+    return fail(SP_ERR_RUNTIME, e.what());
+  }
+}
+
+int ref_compare_csv(int32_t n, const sp_scenario* cs, const int32_t* kinds, const int64_t* const* lengths,
+                    const sp_task* const* ops, const int64_t* const* counts, int32_t allow_mixed, char* buf,
+                    size_t* len) {
+  try {
+    std::vector<SimReport> reps;
+    for (int32_t i = 0; i < n; ++i) {
+      auto cfg = cfg_of(&cs[i]);
+      reps.push_back(simulate(sched_of(cfg, kinds[i], ops[i], counts[i]), part_of(cfg, lengths[i])));
+    }
+    return text_out(compare(reps, allow_mixed != 0).to_csv(), buf, len);
+  } catch (const std::invalid_argument& e) {
+    return fail(SP_ERR_INVALID_ARGUMENT, e.what());
   } catch (const std::exception& e) {
     return fail(SP_ERR_RUNTIME, e.what());
   }

@@ -151,6 +151,11 @@ _SIGS = {
     "sp_schedule_from_json": (C.c_int, [C.c_char_p, P(Scenario), P(C.c_int32), C.c_void_p, C.c_void_p, C.c_int32]),
     "sp_report_to_json": (C.c_int, [P(Scenario), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
                                     C.c_char_p, P(C.c_size_t)]),
+    "sp_render_gantt": (C.c_int, [P(Scenario), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                  C.c_char_p, P(C.c_size_t)]),
+    "sp_compare_csv": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                 C.c_char_p, P(C.c_size_t)]),
+    "sp_engine_render_gantt": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, P(C.c_size_t)]),
     "sp_norm_fwd": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                               C.c_int64, C.c_int32, C.c_float, C.c_void_p]),
     "sp_norm_bwd": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

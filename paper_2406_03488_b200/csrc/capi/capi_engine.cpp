@@ -9,6 +9,7 @@
 #include "engine/comm_plan.hpp"
 #include "engine/engine.hpp"
 #include "seqpipe/json_io.hpp"
+#include "seqpipe/render.hpp"
 #include "seqpipe_b200.h"
 
 struct sp_engine {
@@ -183,6 +184,24 @@ int sp_engine_report_json(sp_engine* eng, int32_t indent, int64_t memory_downsam
   return eguard([&] {
     const std::string text = seqpipe::report_to_json(E(eng).measured_report(), indent,
                                                      static_cast<std::size_t>(memory_downsample < 0 ? 0 : memory_downsample));
+    if (!len) throw std::invalid_argument("null length");
+    const size_t need = text.size() + 1;
+    if (!buf || *len < need) {
+      *len = need;
+      if (buf) throw std::length_error("buffer too small");
+      return;
+    }
+    std::memcpy(buf, text.c_str(), need);
+    *len = need;
+  });
+}
+
+int sp_engine_render_gantt(sp_engine* eng, int32_t format, int32_t width, char* buf, size_t* len) {
+  return eguard([&] {
+    if (format != SP_RENDER_ASCII && format != SP_RENDER_SVG) throw std::invalid_argument("unknown render format");
+    const seqpipe::SimReport rep = E(eng).measured_report();
+    const std::string text =
+        format == SP_RENDER_SVG ? seqpipe::render_svg_gantt(rep) : seqpipe::render_ascii_gantt(rep, width);
     if (!len) throw std::invalid_argument("null length");
     const size_t need = text.size() + 1;
     if (!buf || *len < need) {

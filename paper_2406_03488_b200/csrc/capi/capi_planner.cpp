@@ -10,6 +10,7 @@
 #include "seqpipe/scenario.hpp"
 #include "seqpipe/schedule.hpp"
 #include "seqpipe/json_io.hpp"
+#include "seqpipe/render.hpp"
 #include "seqpipe/sim.hpp"
 #include "seqpipe/validate.hpp"
 #include "seqpipe_b200.h"
@@ -416,6 +417,37 @@ int sp_report_to_json(const sp_scenario* cfg, int32_t kind, const int64_t* lengt
     const auto rep = seqpipe::simulate(schedule_from_c(c, kind, ops, counts), partition_from_c(c, lengths, c.segments));
     return write_text(seqpipe::report_to_json(rep, indent, static_cast<std::size_t>(memory_downsample < 0 ? 0 : memory_downsample)),
                       buf, len);
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int sp_render_gantt(const sp_scenario* cfg, int32_t kind, const int64_t* lengths, const sp_task* ops,
+                    const int64_t* counts, int32_t format, int32_t width, char* buf, size_t* len) {
+  try {
+    const auto c = from_c(cfg);
+    const auto rep = seqpipe::simulate(schedule_from_c(c, kind, ops, counts), partition_from_c(c, lengths, c.segments));
+    if (format != SP_RENDER_ASCII && format != SP_RENDER_SVG) throw std::invalid_argument("unknown render format");
+    return write_text(format == SP_RENDER_SVG ? seqpipe::render_svg_gantt(rep) : seqpipe::render_ascii_gantt(rep, width),
+                      buf, len);
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int sp_compare_csv(int32_t n, const sp_scenario* cfgs, const int32_t* kinds, const int64_t* const* lengths,
+                   const sp_task* const* ops, const int64_t* const* counts, int32_t allow_mixed, char* buf,
+                   size_t* len) {
+  try {
+    if (n < 0 || (n > 0 && (!cfgs || !kinds || !lengths || !ops || !counts))) throw std::invalid_argument("null input");
+    std::vector<seqpipe::SimReport> reps;
+    reps.reserve(static_cast<std::size_t>(n));
+    for (int32_t i = 0; i < n; ++i) {
+      const auto c = from_c(&cfgs[i]);
+      reps.push_back(seqpipe::simulate(schedule_from_c(c, kinds[i], ops[i], counts[i]),
+                                       partition_from_c(c, lengths[i], c.segments)));
+    }
+    return write_text(seqpipe::compare(reps, allow_mixed != 0).to_csv(), buf, len);
   } catch (...) {
     return map_exception();
   }

@@ -28,14 +28,45 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait suspend-time hint (ns): a waiting thread sleeps until the phase
+// completes (or the hint expires) instead of re-issuing the probe -- spinning
+// warps burn issue slots and power on kernels that run power-capped.
+#ifndef SPK_WAIT_HINT
+#define SPK_WAIT_HINT 0
+#endif
+#if SPK_WAIT_HINT
+#define SPK_TRY_WAIT(scope) "mbarrier.try_wait.parity" scope ".shared::cta.b64 p, [%0], %1, " SPK_STR(SPK_WAIT_HINT) ";\n\t"
+#define SPK_TRY_WAIT_W "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, " SPK_STR(SPK_WAIT_HINT) ";\n\t"
+#else
+#define SPK_TRY_WAIT(scope) "mbarrier.try_wait.parity" scope ".shared::cta.b64 p, [%0], %1;\n\t"
+#define SPK_TRY_WAIT_W "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#endif
+#define SPK_STR2(x) #x
+#define SPK_STR(x) SPK_STR2(x)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "WAIT_%=:\n\t" SPK_TRY_WAIT("")
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// Wait with cluster-scope acquire (the phase was completed by arrivals of other CTAs).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t" SPK_TRY_WAIT(".acquire.cluster")
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Arrive (release, cluster scope) on the same-offset barrier of CTA `cta` of the cluster.
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
 // Non-blocking probe: true once the phase with `parity` has completed.
@@ -203,8 +234,7 @@ __device__ __forceinline__ void mbar_wait_w(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   do {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "{\n\t.reg .pred p;\n\t" SPK_TRY_WAIT_W
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity)

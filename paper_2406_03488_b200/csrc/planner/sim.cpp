@@ -4,6 +4,7 @@
 // previous end, so the event loop below gives the reference's times exactly
 // regardless of the order devices are visited in.
 #include <algorithm>
+#include <array>
 #include <map>
 #include <sstream>
 
@@ -242,6 +243,50 @@ std::vector<std::pair<int, int>> replay_order(const Schedule& sch) {
     if (!moved) throw DeadlockError("replay_order: schedule cannot complete (dependency cycle across device orders)");
   }
   return out;
+}
+
+ComparisonTable compare(const std::vector<SimReport>& reports, bool allow_mixed) {
+  if (reports.size() < 2) throw std::invalid_argument("compare needs at least two reports");
+  const ScenarioConfig& base = reports.front().config;
+  const bool same_workload = std::all_of(reports.begin(), reports.end(), [&](const SimReport& r) {
+    return r.config.seq_len == base.seq_len && r.config.micro_batches == base.micro_batches;
+  });
+  if (!allow_mixed && !same_workload)
+    throw std::invalid_argument(
+        "reports cover different workloads (seq_len/micro_batches); pass allow_mixed to override");
+  ComparisonTable table;
+  table.rows.reserve(reports.size());
+  for (const SimReport& r : reports)
+    table.rows.push_back(ComparisonRow{schedule_kind_name(r.kind), r.config, r.makespan, r.aggregate_bubble_ratio,
+                                       r.max_peak_memory, r.modeled_throughput});
+  return table;
+}
+
+std::string ComparisonTable::to_csv() const {
+  std::string csv =
+      "kind,pipeline_size,stages_per_device,micro_batches,segments,seq_len,"
+      "makespan,bubble_ratio,max_peak_memory,throughput,"
+      "makespan_vs_first,bubble_vs_first,memory_vs_first,throughput_vs_first\n";
+  if (rows.empty()) return csv;
+  const ComparisonRow& first = rows.front();
+  auto metrics = [](const ComparisonRow& r) {
+    return std::array<const Rational*, 4>{&r.makespan, &r.bubble_ratio, &r.max_peak_memory, &r.throughput};
+  };
+  const auto base = metrics(first);
+  for (const ComparisonRow& r : rows) {
+    const ScenarioConfig& c = r.config;
+    csv += r.kind;
+    for (long long v : {static_cast<long long>(c.pipeline_size), static_cast<long long>(c.stages_per_device),
+                        static_cast<long long>(c.micro_batches), static_cast<long long>(c.segments),
+                        static_cast<long long>(c.seq_len)})
+      csv += ',' + std::to_string(v);
+    const auto m = metrics(r);
+    for (const Rational* v : m) csv += ',' + format_decimal(*v, 6);
+    for (std::size_t i = 0; i < m.size(); ++i)
+      csv += ',' + (base[i]->is_zero() ? std::string() : format_decimal(*m[i] / *base[i], 6));
+    csv += '\n';
+  }
+  return csv;
 }
 
 }  // namespace seqpipe

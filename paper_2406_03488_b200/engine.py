@@ -113,6 +113,15 @@ class Engine:
         _check(_capi.lib().sp_engine_report_json(self._h, indent, memory_downsample, b, C.byref(n)))
         return b.value.decode()
 
+    def render_gantt(self, fmt: str = "ascii", width: int = 120) -> str:
+        """The last MEASURED step (ns times) drawn by the reference renderers' rules (needs FLAG_TIMELINE)."""
+        n = C.c_size_t(0)
+        f = pl.RENDER_FORMATS[fmt]
+        _check(_capi.lib().sp_engine_render_gantt(self._h, f, width, None, C.byref(n)))
+        b = C.create_string_buffer(n.value)
+        _check(_capi.lib().sp_engine_render_gantt(self._h, f, width, b, C.byref(n)))
+        return b.value.decode()
+
     def op_log(self) -> pl.Schedule:
         P = self.cfg.pipeline_size
         counts = (C.c_int64 * P)()

@@ -550,3 +550,38 @@ def report_to_json(schedule: Schedule, partition: SequencePartition, indent: int
     ops, counts = schedule.flat()
     return _text_out(_capi.lib().sp_report_to_json, C.byref(c), kind_id(schedule.kind), _lengths(partition), ops,
                      counts, indent, memory_downsample)
+
+
+RENDER_FORMATS = {"ascii": 0, "svg": 1}
+
+
+def render_gantt(schedule: Schedule, partition: SequencePartition, fmt: str = "ascii", width: int = 120) -> str:
+    """Timeline of simulate(schedule, partition): render_ascii_gantt (width cells per device row) or
+    render_svg_gantt (reference render.hpp:15-21, render.cpp:46-124)."""
+    c = schedule.config.to_c()
+    ops, counts = schedule.flat()
+    return _text_out(_capi.lib().sp_render_gantt, C.byref(c), kind_id(schedule.kind), _lengths(partition), ops, counts,
+                     RENDER_FORMATS[fmt], width)
+
+
+def _compare_args(runs):
+    n = len(runs)
+    cfgs = (_capi.Scenario * max(1, n))()
+    kinds = (C.c_int32 * max(1, n))()
+    keep, lens, opss, cnts = [], (C.c_void_p * max(1, n))(), (C.c_void_p * max(1, n))(), (C.c_void_p * max(1, n))()
+    for i, (sch, part) in enumerate(runs):
+        cfgs[i] = sch.config.to_c()
+        kinds[i] = kind_id(sch.kind)
+        ops, counts = sch.flat()
+        ls = _lengths(part)
+        keep += [ops, counts, ls]
+        lens[i], opss[i], cnts[i] = C.addressof(ls), C.addressof(ops), C.addressof(counts)
+    return n, cfgs, kinds, lens, opss, cnts, keep
+
+
+def compare_csv(runs, allow_mixed: bool = False) -> str:
+    """compare() of the simulations of [(schedule, partition), ...] as ComparisonTable::to_csv
+    (reference sim.hpp:82-99, sim.cpp:319-367). Raises InvalidArgument for < 2 runs or mixed
+    workloads without allow_mixed."""
+    n, cfgs, kinds, lens, opss, cnts, _keep = _compare_args(runs)
+    return _text_out(_capi.lib().sp_compare_csv, n, cfgs, kinds, lens, opss, cnts, int(allow_mixed))

@@ -179,6 +179,15 @@ def test_measured_report_and_executed_schedule_json(gpu):
         assert dev["warmup_forward_tasks"] == mod["warmup_forward_tasks"]
         assert dev["peak_allocations"] == mod["peak_allocations"]
         assert int(dev["peak_memory"].split("/")[0]) > 0
+    # the measured timeline through the reference renderers' rules (render.cpp:46-124)
+    txt = eng.render_gantt("ascii", 100)
+    rows = txt.splitlines()
+    assert rows[0].startswith("kind=seq1f1b makespan=") and len(rows) == 1 + cfg.pipeline_size
+    assert all(r.startswith(f"device {d + 1} |") and len(r) == len(f"device {d + 1} |") + 101
+               for d, r in enumerate(rows[1:]))
+    assert all(set(r.split("|")[1]) & {"F", "B"} for r in rows[1:])
+    svg = eng.render_gantt("svg")
+    assert svg.count('stroke="#ffffff"') == sum(len(o) for o in log.device_orders) and svg.endswith("</svg>\n")
     eng.close()
 
 
