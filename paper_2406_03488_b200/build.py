@@ -20,6 +20,8 @@ CSRC = PKG / "csrc"
 OUT = PKG / "lib"
 OBJ = PKG / "build_obj"
 LIB = OUT / "libseqpipe_b200.so"
+CLI_SRC = PKG / "cli" / "seqpipe_main.cpp"
+CLI = PKG / "bin" / "seqpipe_b200"
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA / "bin" / "nvcc")
 
@@ -92,8 +94,13 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
     with cf.ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
         objs = list(ex.map(lambda s: _compile(s, digest, verbose), srcs))
     newest = max(o.stat().st_mtime for o in objs)
-    if LIB.exists() and LIB.stat().st_mtime >= newest:
-        return LIB
+    if not (LIB.exists() and LIB.stat().st_mtime >= newest):
+        _link(objs, verbose)
+    _build_cli(verbose)
+    return LIB
+
+
+def _link(objs, verbose: bool) -> None:
     cmd = [
         NVCC, "-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a",
         *map(str, objs), "-o", str(LIB),
@@ -105,7 +112,20 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed\n{r.stdout}\n{r.stderr}")
-    return LIB
+
+
+def _build_cli(verbose: bool) -> None:
+    """bin/seqpipe_b200: the command-line front end, linked against the library (rpath ../lib)."""
+    CLI.parent.mkdir(exist_ok=True)
+    if CLI.exists() and CLI.stat().st_mtime >= max(LIB.stat().st_mtime, CLI_SRC.stat().st_mtime):
+        return
+    cmd = ["g++", *[f for f in CXXFLAGS if f != "-fPIC"], *INCLUDES, str(CLI_SRC), "-o", str(CLI),
+           f"-L{OUT}", "-lseqpipe_b200", "-Wl,-rpath,$ORIGIN/../lib", f"-L{CUDA / 'lib64'}", "-lcudart"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed\n{r.stdout}\n{r.stderr}")
 
 
 if __name__ == "__main__":
