@@ -229,7 +229,7 @@ __device__ __forceinline__ float2 ex2x2_sel(bool poly, float2 v) { return poly ?
 #define SPK_FWD_TURN 0  // measured slower at hd 80 (variant sweep); forward tiles alternate their exponentials: 0 off, 1 before exp, 2 whole block
 #endif
 #ifndef SPK_POLY_FWD
-#define SPK_POLY_FWD 3
+#define SPK_POLY_FWD 2
 #endif
 #ifndef SPK_POLY_BWD
 #define SPK_POLY_BWD 0
