@@ -1183,28 +1183,38 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dq_k(const __grid_constant__ 
 }
 
 // ld: per head, blocks of 64 queries laid out as [64 x -LSE*log2e][64 x -delta],
-// delta = sum_d dO*O; zeros up to n_pad. One warp per (i, head). The dK/dV
-// kernel bulk-copies one 512-byte block per 64-query step.
+// delta = sum_d dO*O; zeros up to n_pad. One thread per (query, head), heads
+// fastest: a warp reads whole 16-byte vectors of one query row (coalesced through
+// L1), each thread reduces its own head in registers. The dK/dV kernel
+// bulk-copies one 512-byte block per 64-query step.
+template <int HD>
 __global__ void attn_prep_k(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                            const float* __restrict__ lse, float* __restrict__ ld, int64_t n, int64_t n_pad, int H,
-                            int hd) {
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (w >= n_pad * H) return;
-  const int head = static_cast<int>(w / n_pad);
-  const int64_t i = w % n_pad;
+                            const float* __restrict__ lse, float* __restrict__ ld, int64_t n, int64_t n_pad, int H) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_pad * H) return;
+  const int64_t i = t / H;
+  const int head = static_cast<int>(t % H);
   float d = 0.f, l = 0.f;
   if (i < n) {
-    const int64_t base = i * (int64_t)H * hd + head * hd;
-    for (int c = lane; c < hd; c += 32) d += __bfloat162float(o[base + c]) * __bfloat162float(dout[base + c]);
-    d = warp_sum(d);
+    const uint4* ov = reinterpret_cast<const uint4*>(o + i * (int64_t)H * HD + head * HD);
+    const uint4* dv = reinterpret_cast<const uint4*>(dout + i * (int64_t)H * HD + head * HD);
+#pragma unroll
+    for (int c = 0; c < HD / 8; ++c) {
+      const uint4 a = ov[c], b = dv[c];
+      const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&aw[k]));
+        const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bw[k]));
+        d = fmaf(fa.x, fb.x, d);
+        d = fmaf(fa.y, fb.y, d);
+      }
+    }
     l = lse[(int64_t)head * n + i] * 1.4426950408889634f;
   }
-  if (lane == 0) {
-    const int64_t at = (head * n_pad + (i & ~int64_t(63))) * 2 + (i & 63);
-    ld[at] = -l;
-    ld[at + 64] = -d;
-  }
+  const int64_t at = (head * n_pad + (i & ~int64_t(63))) * 2 + (i & 63);
+  ld[at] = -l;
+  ld[at + 64] = -d;
 }
 
 // ---------------------------------------------------------------------------- host
@@ -1275,14 +1285,20 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
                  cudaStream_t s) {
   const int h = H * hd;
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kv) | reinterpret_cast<uintptr_t>(dout) |
-       reinterpret_cast<uintptr_t>(dq) | reinterpret_cast<uintptr_t>(dkv)) & 15)
+       reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(dq) | reinterpret_cast<uintptr_t>(dkv)) & 15)
     throw std::invalid_argument("attention: operands must be 16-byte aligned");
   (void)ws_dq;
   const int64_t n_pad = (n + 127) / 128 * 128;  // the dQ kernel reads whole 128-row blocks
   {
-    const int64_t warps = n_pad * H;
-    attn_prep_k<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, ws_delta, n, n_pad, H, hd);
+    const unsigned blocks = static_cast<unsigned>((n_pad * H + 255) / 256);
+    const auto* ob = static_cast<const __nv_bfloat16*>(o);
+    const auto* db = static_cast<const __nv_bfloat16*>(dout);
+    switch (hd) {
+      case 64: attn_prep_k<64><<<blocks, 256, 0, s>>>(ob, db, lse, ws_delta, n, n_pad, H); break;
+      case 80: attn_prep_k<80><<<blocks, 256, 0, s>>>(ob, db, lse, ws_delta, n, n_pad, H); break;
+      case 128: attn_prep_k<128><<<blocks, 256, 0, s>>>(ob, db, lse, ws_delta, n, n_pad, H); break;
+      default: throw std::invalid_argument("attention: unsupported head_dim");
+    }
     SPK_LAUNCH_CHECK();
   }
   // dKV kernel: Q/dO tiles of 64 rows, K/V tiles of 128 rows; dQ kernel: the reverse.

@@ -447,6 +447,25 @@ __global__ void __launch_bounds__(256) norm_bwd_vec_k(const __nv_bfloat16* __res
 
 __device__ __forceinline__ float gelu_f(float u) { return gelu_tanh(u); }
 
+// bf16 production path: MUFU tanh (tanh.approx.f32, max rel. error ~2^-11, far
+// below the bf16 output rounding). libm tanhf made these HBM-sized kernels
+// issue-bound (~20 instructions per element). The fp32 validation path keeps tanhf.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu_fast(float u) {
+  const float c = 0.7978845608028654f;
+  return 0.5f * u * (1.f + tanh_fast(c * (u + 0.044715f * u * u * u)));
+}
+__device__ __forceinline__ float gelu_grad_fast(float u) {
+  const float c = 0.7978845608028654f;
+  const float t = tanh_fast(c * (u + 0.044715f * u * u * u));
+  return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * u * u);
+}
+__device__ __forceinline__ float sigmoid_fast(float u) { return fmaf(0.5f, tanh_fast(0.5f * u), 0.5f); }
+
 // GeLU (family 0) / SwiGLU (family 1) over 8-element vectors.
 __global__ void act_fwd_vec_k(int family, const __nv_bfloat16* __restrict__ u, __nv_bfloat16* __restrict__ g,
                               int64_t n, int F) {
@@ -456,14 +475,14 @@ __global__ void act_fwd_vec_k(int family, const __nv_bfloat16* __restrict__ u, _
     if (family == 0) {
       bf8_to_f(reinterpret_cast<const Bf8*>(u)[i], a);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) a[e] = gelu_tanh(a[e]);
+      for (int e = 0; e < 8; ++e) a[e] = gelu_fast(a[e]);
     } else {
       const int64_t r = i / per_row, c = i % per_row;
       float b[8];
       bf8_to_f(reinterpret_cast<const Bf8*>(u)[r * 2 * per_row + c], a);
       bf8_to_f(reinterpret_cast<const Bf8*>(u)[r * 2 * per_row + per_row + c], b);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) a[e] = a[e] * sigmoidf_(a[e]) * b[e];
+      for (int e = 0; e < 8; ++e) a[e] = a[e] * sigmoid_fast(a[e]) * b[e];
     }
     reinterpret_cast<Bf8*>(g)[i] = f_to_bf8(a);
   }
@@ -479,7 +498,7 @@ __global__ void act_bwd_vec_k(int family, const __nv_bfloat16* __restrict__ u, c
       float a[8];
       bf8_to_f(reinterpret_cast<const Bf8*>(u)[i], a);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) a[e] = d[e] * gelu_tanh_grad(a[e]);
+      for (int e = 0; e < 8; ++e) a[e] = d[e] * gelu_grad_fast(a[e]);
       reinterpret_cast<Bf8*>(du)[i] = f_to_bf8(a);
     } else {
       const int64_t r = i / per_row, c = i % per_row;
@@ -488,7 +507,7 @@ __global__ void act_bwd_vec_k(int family, const __nv_bfloat16* __restrict__ u, c
       bf8_to_f(reinterpret_cast<const Bf8*>(u)[r * 2 * per_row + per_row + c], b);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float s = sigmoidf_(a[e]);
+        const float s = sigmoid_fast(a[e]);
         const float da = d[e] * b[e] * s * (1.f + a[e] * (1.f - s)), db = d[e] * a[e] * s;
         a[e] = da;
         b[e] = db;
