@@ -29,7 +29,9 @@ def _rel(a, b):
 
 @pytest.mark.parametrize("a_k,b_k", [(1, 1), (1, 0), (0, 0), (0, 1)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (304, 520, 200), (1037, 768, 2560), (2048, 2560, 10170), (2100, 2380, 300),
-                                   (10170, 7680, 2560)])
+                                   (10170, 7680, 2560),
+                                   # weight-gradient shapes (few tiles, long K)
+                                   (2560, 2560, 6674), (7680, 2560, 8496), (300, 520, 4100)])
 def test_tcgen05_gemm_layouts(gpu, a_k, b_k, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
     A = torch.randn((M, K) if a_k else (K, M), device="cuda", generator=g).to(torch.bfloat16)

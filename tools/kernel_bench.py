@@ -99,6 +99,8 @@ def main():
             "mlp_up_dgrad": (n, h, F, 1, 0, 0, 0),
             "mlp_up_wgrad": (F, h, n, 0, 0, 1, 1),
             "qkv_wgrad": (3 * h, h, n, 0, 0, 1, 1),
+            "o_wgrad": (h, h, n, 0, 0, 1, 1),
+            "mlp_down_wgrad": (h, F, n, 0, 0, 1, 1),
         }.items():
             ms, tf = gemm_case(M, N, K, ak, bk, cf, acc)
             print(json.dumps({"kernel": "gemm_tcgen05", "model": name, "role": role, "M": M, "N": N, "K": K,
