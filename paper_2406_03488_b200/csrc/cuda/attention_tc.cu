@@ -228,6 +228,15 @@ __device__ __forceinline__ float2 ex2x2_sel(bool poly, float2 v) { return poly ?
 #ifndef SPK_FWD_TURN
 #define SPK_FWD_TURN 0  // measured slower at hd 80 (variant sweep); forward tiles alternate their exponentials: 0 off, 1 before exp, 2 whole block
 #endif
+#ifndef SPK_DKV_NS
+#define SPK_DKV_NS 3  // hd <= 80 dK/dV: score buffers (the dP^T buffers take the remaining 4 - NS)
+#endif
+#ifndef SPK_DQ_NS
+#define SPK_DQ_NS 3  // hd <= 80 dQ: score / dP buffers
+#endif
+#ifndef SPK_DQ_ND
+#define SPK_DQ_ND 1
+#endif
 #ifndef SPK_POLY_FWD
 #define SPK_POLY_FWD 2
 #endif
@@ -633,7 +642,7 @@ struct __align__(64) AttnBwdParams {
 template <int HD>
 struct DkvCfg {
   static constexpr bool KVT = HD <= 80;  // K, V in TMEM (hd 128: no room; SS form)
-  static constexpr int NS = KVT ? 3 : 2, ND = KVT ? 1 : 2;
+  static constexpr int NS = KVT ? SPK_DKV_NS : 2, ND = KVT ? 4 - SPK_DKV_NS : 2;
   static constexpr uint32_t T_DP = NS * 64, T_DV = T_DP + ND * 64;
   static constexpr uint32_t T_DK = T_DV + (HD == 80 ? 96 : HD);
   static constexpr uint32_t T_K = T_DK + HD, T_V = T_K + HD / 2;
@@ -641,7 +650,7 @@ struct DkvCfg {
 };
 template <int HD>
 struct DqCfg {
-  static constexpr int NS = HD == 128 ? 2 : 3, ND = HD == 128 ? 2 : 1;
+  static constexpr int NS = HD == 128 ? 2 : SPK_DQ_NS, ND = HD == 128 ? 2 : SPK_DQ_ND;
   static constexpr uint32_t T_DP = NS * 64, T_DQ = T_DP + ND * 64;
   static constexpr uint32_t T_Q = T_DQ + (HD == 80 ? 96 : HD), T_DO = T_Q + HD / 2;
   static_assert(T_DO + HD / 2 <= 512, "dQ TMEM budget");
