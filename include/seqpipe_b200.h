@@ -22,6 +22,8 @@
  *   sp_check_schedule / sp_check_warmup     core/include/seqpipe/validate.hpp:34,42, core/src/validate.cpp:85-325
  *   sp_schedule_to_json / _from_json        core/include/seqpipe/json_io.hpp:19-20, core/src/json_io.cpp:59-97
  *   sp_report_to_json                       core/include/seqpipe/json_io.hpp:25-26, core/src/json_io.cpp:99-159
+ *   sp_render_gantt / sp_engine_render_gantt  core/include/seqpipe/render.hpp:15-21, core/src/render.cpp:46-124
+ *   sp_compare_csv                          core/include/seqpipe/sim.hpp:82-99, core/src/sim.cpp:319-367
  *   sp_device_partition / sp_device_schedule_ops   GPU-resident launcher core (no reference counterpart;
  *                                           bit-exact with cwp_partition/generate)
  *   sp_engine_*                             replaces the modeled execution of simulate() (sim.cpp:121-317)
