@@ -12,6 +12,14 @@ from oracle import ref
 pytestmark = pytest.mark.gpu
 CLI = Path(__file__).resolve().parent.parent / "paper_2406_03488_b200" / "bin" / "seqpipe_b200"
 
+
+@pytest.fixture(scope="module", autouse=True)
+def _cli_built():
+    if not CLI.exists():  # snapshot without the binary: link it against the shipped library (g++ only)
+        from paper_2406_03488_b200 import build as B
+        B._build_cli(verbose=False)
+    assert CLI.exists()
+
 TINY = """pipeline_size = 4
 stages_per_device = 1
 micro_batches = 6
