@@ -1207,10 +1207,10 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dq_k(const __grid_constant__ 
 // x N = 80 x K = 128 keys MMA group accumulates dQ in TMEM, which the softmax warps
 // drain one pair later with red.global.add.v4.f32 into an fp32 [n, h] workspace
 // (summed over the key tiles; the host scales and casts it into dq).
-// TMEM: S^T [2] x 64 | dP^T 64 | dV 96 | dQ 96 | dK 80 | V 40 (bf16 pairs).
+// TMEM: S^T [2] x 64 | dP^T 64 | dV 80 | dQ 80 | dK 80 | K 40 | V 40 (bf16 pairs).
 struct FusedCfg {
   static constexpr int NS = 2, ND = 1;
-  static constexpr uint32_t T_DP = 128, T_DV = 192, T_DQ = 288, T_DK = 384, T_V = 464;
+  static constexpr uint32_t T_DP = 128, T_DV = 192, T_DQ = 272, T_DK = 352, T_K = 432, T_V = 472;
 };
 constexpr int FUSED_DS_T = 2 * 128 * 128;  // one dS^T tile: 2 query halves x 128 keys x 128 B
 template <int HD>
@@ -1360,7 +1360,9 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_fused_k(const __grid_constant
           tc::mma_bf16_ts_w(tmem + C::T_DP, tmem + C::T_V + 8 * kk, kdesc<HD>(do_base, 64, kk), idesc_s, kk > 0);
         tc::mma_commit_w(dp_full);
       }
-    } else if (warp == 3) {  // S^T = K Q^T (A = K tile in SMEM)
+    } else if (warp == 3) {  // S^T = K Q^T (A = K copied into TMEM)
+      tc::mbar_wait_w(v_tmem, 0);
+      tc::tc_fence_after();
       for (int it = 0; it < niter; ++it) {
         const int st = it % QST;
         if (it >= NS) tc::mbar_wait_w(&s_free[it % NS], ((it / NS) - 1) & 1);
@@ -1369,8 +1371,7 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_fused_k(const __grid_constant
         const uint32_t q_base = tc::smem_u32(sQ + st * Q_T);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
-          tc::mma_bf16_ss_w(tmem + (it % NS) * 64, kdesc<HD>(k_base, 128, kk), kdesc<HD>(q_base, 64, kk), idesc_s,
-                            kk > 0);
+          tc::mma_bf16_ts_w(tmem + (it % NS) * 64, tmem + C::T_K + 8 * kk, kdesc<HD>(q_base, 64, kk), idesc_s, kk > 0);
         tc::mma_commit_w(&s_full[it % NS]);
       }
     } else {  // dV += P^T dO, dK += dS^T Q; after each odd block: dQ(pair) = dS K
@@ -1409,7 +1410,8 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_fused_k(const __grid_constant
     const int64_t kpos = j0 + r;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     tc::mbar_wait(kv_full, 0);
-    if (g < 2) row_part_smem_to_tmem<HD>(tmem + lane_base + C::T_V + g * (HD / 4), sV, 128, r, g);
+    row_part_smem_to_tmem<HD>(tmem + lane_base + (g < 2 ? C::T_V : C::T_K) + (g & 1) * (HD / 4), g < 2 ? sV : sK, 128,
+                              r, g & 1);  // groups 0/1: V halves, 2/3: K halves (K also stays in SMEM for dQ)
     tc::tmem_st_wait();
     tc::tc_fence_before();
     warp_arrive(v_tmem);
