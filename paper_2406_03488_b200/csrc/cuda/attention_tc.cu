@@ -628,7 +628,9 @@ struct __align__(64) AttnBwdParams {
   int64_t n, q_off, kv_len;
   int H, h;
   float scale, scale_log2;
-  int dbg;  // profiling only (SP_ATTN_DBG): 1 = skip dK/dV MMAs, 2 = skip the dK/dV softmax (TMEM ld/st + math)
+  int dbg;  // profiling only (SP_ATTN_DBG): 1 = skip dK/dV MMAs, 2 = skip the dK/dV softmax (TMEM ld/st + math);
+            // fused kernel: 16 = skip the dQ reduce, 32 = skip the dQ MMAs, 64 = skip the dS^T staging,
+            // 128 = skip its proxy fence
   unsigned long long* trace;  // profiling only (SP_ATTN_TRACE): cycle stamps of one CTA, [event][iteration]
 };
 
@@ -1277,7 +1279,7 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_fused_k(const __grid_constant
   uint64_t* q_empty = q_full + QST;      // [QST]
   uint64_t* s_free = q_empty + QST;      // [2]
   uint64_t* stage_full = s_free + NS;    // dQ staging tile written (16 softmax warps)
-  uint64_t* stage_free = stage_full + 1; // the reduce of the tile has read it (warp 20)
+  uint64_t* stage_free = stage_full + 1; // the reduce of the tile has read it (warp 4, lane 0)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stage_free + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
