@@ -173,6 +173,15 @@ class Stage {
   float* wm(int64_t off) const { return master_ + off; }
   float* wg(int64_t off) const { return grad_ + off; }
   void gemm(const spk::GemmArgs& a, double flop);
+  // Weight-gradient GEMM on the side stream, concurrent with the dgrad GEMM that
+  // follows it (the two read the same operands and write disjoint outputs); the
+  // persistent kernels then fill each other's last-wave tails. join() makes the
+  // compute stream wait before anything overwrites the wgrad operands.
+  void wgrad(const spk::GemmArgs& a, double flop);
+  void join();
+  cudaStream_t s2_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  bool pending_join_ = false;
   void head_forward_backward(Seg& sg, int m, const int32_t* tokens_dev, double* loss_acc, float loss_scale);
   int64_t add_param(const std::string& name, int rows, int cols);
 

@@ -10,6 +10,7 @@
 //           stage's fp32 dKV accumulator; rows of segment s are then complete
 //           (reverse edge B(m,s+1) -> B(m,s)), feed the QKV weight/input grads.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
@@ -176,6 +177,9 @@ Stage::Stage(const ModelCfg& m, const seqpipe::ScenarioConfig& cfg, const std::v
 }
 
 Stage::~Stage() {
+  if (s2_) cudaStreamDestroy(s2_);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
   for (void* p : {(void*)master_, (void*)grad_, (void*)adam_m_, (void*)adam_v_, w_a_, w_big1_, w_big2_, w_t1_, w_t2_,
                   w_t3_, w_dqkv_, (void*)w_delta_, (void*)w_dq_, (void*)w_fmean_, (void*)w_frstd_, w_logits_,
                   (void*)dkv_, (void*)arena_ptr_})
@@ -360,6 +364,36 @@ void* Stage::kv(int m, int layer) const {
   const int64_t off = kv_off_[m - 1];
   if (off < 0) throw std::logic_error("KV slab not planned");
   return arena_ptr_ + off + static_cast<int64_t>(layer) * T_ * 2 * mc_.h * esz_;
+}
+
+void Stage::wgrad(const GemmArgs& a, double flop) {
+  static const bool side = [] {
+    const char* e = std::getenv("SP_WGRAD_STREAM");  // tuning: 0 = weight gradients in stream order
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  // Kernel probes time each GEMM on the compute stream; keep stream order then.
+  if (!side || (probe && probe->enabled) || (mc_.flags & SP_FLAG_NO_TCGEN05) || mc_.dt == DType::kF32) {
+    gemm(a, flop);
+    return;
+  }
+  if (!s2_) {
+    SPK_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
+    SPK_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    SPK_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  }
+  SPK_CUDA(cudaEventRecord(ev_fork_, s_));
+  SPK_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
+  spk::gemm(a, s2_, spk::kGemmAuto);
+  SPK_CUDA(cudaEventRecord(ev_join_, s2_));
+  pending_join_ = true;
+  flops += flop;
+  ++launches;
+}
+
+void Stage::join() {
+  if (!pending_join_) return;
+  SPK_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
+  pending_join_ = false;
 }
 
 void Stage::gemm(const GemmArgs& a, double flop) {
@@ -567,18 +601,20 @@ void Stage::backward_impl(int m, int s, void* dx_target, const int32_t* tokens, 
     } else {
       g = G(dt, h, F, n, dy, h, false, w_big1_, F, false, wg(w.w2), F, DType::kF32);
       g.epi = Epi::kAccumF32;
-      gemm(g, 2.0 * n * h * F);
+      wgrad(g, 2.0 * n * h * F);
     }
     gemm(G(dt, n, F, h, dy, h, true, wc(w.w2), F, false, w_big2_, F, dt), 2.0 * n * h * F);
+    join();  // act_bwd overwrites w_big1_
     spk::act_bwd(dt, mc_.family, sg.u[l], w_big2_, w_big1_, n, F, s_);
     if (defer_w) {
       SPK_CUDA(cudaMemcpyAsync(sg.w_du[l], w_big1_, esz_ * n * Fu, cudaMemcpyDeviceToDevice, s_));
     } else {
       g = G(dt, Fu, h, n, w_big1_, Fu, false, w_a_, h, false, wg(w.w1), h, DType::kF32);
       g.epi = Epi::kAccumF32;
-      gemm(g, 2.0 * n * Fu * h);
+      wgrad(g, 2.0 * n * Fu * h);
     }
     gemm(G(dt, n, h, Fu, w_big1_, Fu, true, wc(w.w1), h, false, w_t1_, h, dt), 2.0 * n * Fu * h);
+    join();
     spk::norm_bwd(dt, mc_.rms(), w_t1_, sg.x_mid[l], wm(w.norm2), sg.mean2[l], sg.rstd2[l], dy, w_t2_, wg(w.norm2), n,
                   mc_.h, s_);
     // ---- attention: x_mid = x + attn(norm1(x)) Wo^T
@@ -587,9 +623,10 @@ void Stage::backward_impl(int m, int s, void* dx_target, const int32_t* tokens, 
     } else {
       g = G(dt, h, h, n, w_t2_, h, false, sg.o[l], h, false, wg(w.wo), h, DType::kF32);
       g.epi = Epi::kAccumF32;
-      gemm(g, 2.0 * n * h * h);
+      wgrad(g, 2.0 * n * h * h);
     }
     gemm(G(dt, n, h, h, w_t2_, h, true, wc(w.wo), h, false, w_t3_, h, dt), 2.0 * n * h * h);
+    join();
     float* dkv_l = dkv(l);
     // Algorithmic count: backward = 2x forward attention FLOPs (SURVEY §8d convention).
     const double attn_flops = 2.0 * 4.0 * h * (static_cast<double>(n) * pos0 + 0.5 * static_cast<double>(n) * n);
@@ -611,9 +648,10 @@ void Stage::backward_impl(int m, int s, void* dx_target, const int32_t* tokens, 
       spk::norm_apply(dt, mc_.rms(), sg.x_in[l], wm(w.norm1), sg.mean1[l], sg.rstd1[l], w_a_, n, mc_.h, s_);
       g = G(dt, 3 * h, h, n, w_dqkv_, 3 * h, false, w_a_, h, false, wg(w.wqkv), h, DType::kF32);
       g.epi = Epi::kAccumF32;
-      gemm(g, 2.0 * n * 3 * h * h);
+      wgrad(g, 2.0 * n * 3 * h * h);
     }
     gemm(G(dt, n, h, 3 * h, w_dqkv_, 3 * h, true, wc(w.wqkv), h, false, w_t1_, h, dt), 2.0 * n * 3 * h * h);
+    join();
     void* dx = (l > 0) ? w_t2_ : (first() ? w_t3_ : dx_target);
     spk::norm_bwd(dt, mc_.rms(), w_t1_, sg.x_in[l], wm(w.norm1), sg.mean1[l], sg.rstd1[l], w_t2_, dx, wg(w.norm1), n,
                   mc_.h, s_);
