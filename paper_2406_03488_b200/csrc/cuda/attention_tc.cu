@@ -1683,6 +1683,28 @@ void attn_fwd_tc(const void* q, const void* kv, void* o, float* lse, int64_t n, 
 
 size_t attn_bwd_ws_delta_floats(int64_t n, int H) { return static_cast<size_t>(H) * ((n + 127) / 128 * 128) * 2; }
 
+// Side stream of the calling thread's device for the dQ kernel: it runs concurrently
+// with the dK/dV kernel (both only read the prep output and write disjoint results),
+// so each fills the other's last-wave tail.
+namespace {
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream() {
+  static thread_local SideStream per_dev[16];
+  int dev = 0;
+  SPK_CUDA(cudaGetDevice(&dev));
+  SideStream& ss = per_dev[dev & 15];
+  if (!ss.s) {
+    SPK_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    SPK_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    SPK_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  }
+  return ss;
+}
+}  // namespace
+
 void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout, const float* lse, float* ws_delta,
                  float* ws_dq, void* dq, float* dkv, int64_t n, int64_t q_off, int64_t kv_len, int H, int hd,
                  cudaStream_t s) {
@@ -1816,6 +1838,22 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
       at[0].val.clusterDim.z = 1;
       lc.attrs = at;
       lc.numAttrs = 1;
+      static const bool concurrent = [] {
+        const char* e = std::getenv("SP_ATTN_BWD_CONCURRENT");  // tuning: 0 = dQ after dK/dV in stream order
+        return e ? std::atoi(e) != 0 : true;
+      }();
+      if (concurrent && !trace_buf) {  // dQ first (long CTAs), on the side stream
+        SideStream& ss = side_stream();
+        SPK_CUDA(cudaEventRecord(ss.fork, s));
+        SPK_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+        dim3 g2c(static_cast<unsigned>((n + 127) / 128), static_cast<unsigned>(H));
+        attn_bwd_dq_k<HD><<<g2c, 640, smem_dq, ss.s>>>(b);
+        SPK_LAUNCH_CHECK();
+        SPK_CUDA(cudaEventRecord(ss.join, ss.s));
+        SPK_CUDA(cudaLaunchKernelEx(&lc, attn_bwd_dkv_k<HD>, a));
+        SPK_CUDA(cudaStreamWaitEvent(s, ss.join, 0));
+        return;
+      }
       SPK_CUDA(cudaLaunchKernelEx(&lc, attn_bwd_dkv_k<HD>, a));
       if (trace_buf) {
         unsigned long long h_t[16 * 64];
