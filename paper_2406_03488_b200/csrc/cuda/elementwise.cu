@@ -1,3 +1,4 @@
+#include <cstdlib>
 // HBM-bound kernels of the per-stage transformer: embedding, LayerNorm/RMSNorm
 // (fwd, recompute, bwd), GeLU/SwiGLU, RoPE, fused cross-entropy, AdamW, init.
 // One CTA per row for the row reductions (warp-shuffle + smem reduce), grid
@@ -445,6 +446,94 @@ __global__ void __launch_bounds__(256) norm_bwd_vec_k(const __nv_bfloat16* __res
   }
 }
 
+// Wide rows (NV >= 8, h >= 2048): two warps per row, each owning one half of the
+// columns (NV/2 16-byte vectors per lane, cached in registers). Half the registers
+// of norm_bwd_vec_k, so two 8-warp CTAs fit per SM and each row's load latency
+// is split over two warps; the row sums are combined through shared memory.
+template <int NV, bool RMS>
+__global__ void __launch_bounds__(256, 2) norm_bwd_pair_k(const __nv_bfloat16* __restrict__ dy,
+                                                          const __nv_bfloat16* __restrict__ x,
+                                                          const float* __restrict__ g, const float* __restrict__ mean,
+                                                          const float* __restrict__ rstd, const __nv_bfloat16* dres,
+                                                          __nv_bfloat16* dx, float* __restrict__ dg, int64_t n) {
+  constexpr int H = 256 * NV, NH = NV / 2, HH = H / 2;
+  extern __shared__ float4 sdg4[];  // [8 warps][H/2] fp32 dgain partials, then [2 parity][4 pairs][2 halves][2]
+  float* sdg = reinterpret_cast<float*>(sdg4);
+  float* xch = sdg + 8 * HH;
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32, pr = w >> 1, hw = w & 1;
+  float* my = sdg + w * HH;
+  for (int c = lane * 4; c < HH; c += 128) *reinterpret_cast<float4*>(my + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncwarp();
+  int par = 0;
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * 4 + pr; row < n;
+       row += static_cast<int64_t>(gridDim.x) * 4, par ^= 1) {
+    const Bf8* xr = reinterpret_cast<const Bf8*>(x + row * H) + hw * NH * 32;
+    const Bf8* dyr = reinterpret_cast<const Bf8*>(dy + row * H) + hw * NH * 32;
+    const float* gh = g + hw * HH;
+    const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
+    Bf8 xv[NH], dv[NH];
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      xv[k] = xr[k * 32 + lane];
+      dv[k] = dyr[k * 32 + lane];
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      float f[8], d[8], gv[8];
+      bf8_to_f(xv[k], f);
+      bf8_to_f(dv[k], d);
+      ld_f8(gh + (k * 32 + lane) * 8, gv);
+      float* acc = my + (k * 32 + lane) * 8;
+      float4 a0 = *reinterpret_cast<float4*>(acc), a1 = *reinterpret_cast<float4*>(acc + 4);
+      float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xh = (f[e] - mu) * rs, dxh = d[e] * gv[e];
+        s1 += dxh;
+        s2 += dxh * xh;
+        av[e] += d[e] * xh;
+      }
+      *reinterpret_cast<float4*>(acc) = make_float4(av[0], av[1], av[2], av[3]);
+      *reinterpret_cast<float4*>(acc + 4) = make_float4(av[4], av[5], av[6], av[7]);
+    }
+    s1 = RMS ? 0.f : warp_sum(s1);
+    s2 = warp_sum(s2);
+    float* slot = xch + ((par * 4 + pr) * 2) * 2;
+    if (lane == 0) {
+      slot[hw * 2] = s1;
+      slot[hw * 2 + 1] = s2;
+    }
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + pr) : "memory");
+    const float m1 = RMS ? 0.f : (s1 + slot[(hw ^ 1) * 2]) / H;
+    const float m2 = (s2 + slot[(hw ^ 1) * 2 + 1]) / H;
+    Bf8* dxr = reinterpret_cast<Bf8*>(dx + row * H) + hw * NH * 32;
+    const Bf8* drr = dres ? reinterpret_cast<const Bf8*>(dres + row * H) + hw * NH * 32 : nullptr;
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      float f[8], d[8], gv[8], r[8];
+      bf8_to_f(xv[k], f);
+      bf8_to_f(dv[k], d);
+      ld_f8(gh + (k * 32 + lane) * 8, gv);
+      if (drr) bf8_to_f(drr[k * 32 + lane], r);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xh = (f[e] - mu) * rs;
+        f[e] = rs * (d[e] * gv[e] - m1 - xh * m2) + (drr ? r[e] : 0.f);
+      }
+      dxr[k * 32 + lane] = f_to_bf8(f);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < H; c += 256) {
+    const int h2 = c / HH, cc = c - h2 * HH;
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s += sdg[(q * 2 + h2) * HH + cc];
+    atomicAdd(&dg[c], s);
+  }
+}
+
 __device__ __forceinline__ float gelu_f(float u) { return gelu_tanh(u); }
 
 // bf16 production path: MUFU tanh (tanh.approx.f32, max rel. error ~2^-11, far
@@ -641,6 +730,28 @@ void norm_bwd(DType t, bool rms, const void* dy, const void* x, const float* g, 
           kern<<<grid, 256, sm, s>>>(static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), g, mean,
                                      rstd, static_cast<const __nv_bfloat16*>(dres), static_cast<__nv_bfloat16*>(dx), dg, n);
         };
+        if constexpr (NV >= 8 && NV <= 12 && NV % 2 == 0) {  // measured: +5 % at h 2560, -8 % at h 4096
+          static const bool pair = [] {
+            const char* e = std::getenv("SP_NORM_BWD_PAIR");  // tuning: 0 = one warp per row
+            return e ? std::atoi(e) != 0 : true;
+          }();
+          if (pair) {
+            const size_t sm2 = sizeof(float) * (8 * 128 * NV + 32);
+            const int64_t b2 = (n + 3) / 4;
+            const unsigned grid2 = static_cast<unsigned>(b2 < 2 * num_sms() ? b2 : 2 * num_sms());
+            auto launch2 = [&](auto kern) {
+              SPK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+              kern<<<grid2, 256, sm2, s>>>(static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), g,
+                                          mean, rstd, static_cast<const __nv_bfloat16*>(dres),
+                                          static_cast<__nv_bfloat16*>(dx), dg, n);
+            };
+            if (rms)
+              launch2(norm_bwd_pair_k<NV, true>);
+            else
+              launch2(norm_bwd_pair_k<NV, false>);
+            return;
+          }
+        }
         if (rms)
           launch(norm_bwd_vec_k<NV, true>);
         else
