@@ -614,6 +614,8 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
 
 struct __align__(64) AttnBwdParams {
   CUtensorMap tdkv;  // dkv fp32 [kv_len, 2h], [128 x HD] boxes (TMA reduce-add of dK / dV)
+  CUtensorMap tdkv32;  // the same tensor, [128 x 32] boxes, 128-byte swizzle (swizzled dK/dV staging)
+  CUtensorMap tdkv16;  // [128 x 16] boxes, 64-byte swizzle (the last 16 columns of head dim 80)
   CUtensorMap tdq;   // dQ fp32 [n, h], [128 x 32] boxes, 128-byte swizzle (fused kernel: TMA reduce-add)
   CUtensorMap tdq16; // the same, [128 x 16] boxes, 64-byte swizzle (head-dim columns 64..79)
   Maps tq;           // q  [n, h]
@@ -970,18 +972,37 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
       tmem_ld16(tmem + lane_base + (is_k ? C::T_DK : C::T_DV) + c * 16, v);
       tc::tmem_ld_wait();
       const float sc = is_k ? p.scale : 1.f;
-      float* dst = out + (is_k ? 0 : 128 * HD) + r * HD + c * 16;
+      // staging = the reduce boxes: 32-column [128 x 128 B] tiles (128-byte swizzle) and,
+      // for head dim 80, a 16-column [128 x 64 B] tile (64-byte swizzle): the per-row
+      // float4 stores are bank-conflict free (a dense [128 x HD] tile is 16-way).
+      uint8_t* tile = reinterpret_cast<uint8_t*>(out + (is_k ? 0 : 128 * HD));
 #pragma unroll
-      for (int e = 0; e < 16; e += 4)
-        *reinterpret_cast<float4*>(dst + e) =
+      for (int e = 0; e < 16; e += 4) {
+        uint8_t* dst;
+        if (c < 2 * (HD / 32)) {
+          const int u = (c & 1) * 4 + e / 4;
+          dst = tile + (c >> 1) * 16384 + r * 128 + ((u ^ (r & 7)) << 4);
+        } else {
+          const int u = e / 4;
+          dst = tile + (HD / 32) * 16384 + r * 64 + ((u ^ ((r >> 1) & 3)) << 4);
+        }
+        *reinterpret_cast<float4*>(dst) =
             make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
                         __uint_as_float(v[e + 3]) * sc);
+      }
     }
     tc::fence_proxy_async_smem();
     tc::named_bar_sync(1, 512);
     if (warp == 4 && lane == 0) {
-      tc::tma_reduce_add_2d(&p.tdkv, out, head * HD, static_cast<int>(j0));
-      tc::tma_reduce_add_2d(&p.tdkv, out + 128 * HD, p.h + head * HD, static_cast<int>(j0));
+#pragma unroll
+      for (int is_v = 0; is_v < 2; ++is_v) {
+        const float* tile = out + is_v * 128 * HD;
+        const int col = (is_v ? p.h : 0) + head * HD;
+#pragma unroll
+        for (int b = 0; b < HD / 32; ++b) tc::tma_reduce_add_2d(&p.tdkv32, tile + b * 4096, col + 32 * b, static_cast<int>(j0));
+        if constexpr (HD % 32 == 16)
+          tc::tma_reduce_add_2d(&p.tdkv16, tile + (HD / 32) * 4096, col + HD - 16, static_cast<int>(j0));
+      }
       tc::bulk_commit();
       tc::bulk_wait_read0();  // SMEM must outlive the copy-out
     }
@@ -1742,6 +1763,15 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
     CUresult r = tma_encode_fn()(&a.tdkv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dkv, dims, strides, box, estr,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cuuint32_t box32[2] = {32, 128}, box16[2] = {16, 128};
+    if (r == CUDA_SUCCESS)
+      r = tma_encode_fn()(&a.tdkv32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dkv, dims, strides, box32, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS)
+      r = tma_encode_fn()(&a.tdkv16, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dkv, dims, strides, box16, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (dkv) failed: " + std::to_string((int)r));
   }
   a.q = static_cast<const __nv_bfloat16*>(q);
