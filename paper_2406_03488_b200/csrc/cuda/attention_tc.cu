@@ -626,6 +626,7 @@ struct __align__(64) AttnBwdParams {
   int64_t n_pad;     // n rounded up to 128
   float* dkv;        // [kv_len, 2h] fp32 accumulator
   float* dqf;        // [n, h] fp32 dQ accumulator (fused kernel; zeroed by the host)
+  int dkv_store;     // dK/dV epilogue writes (TMA store) instead of adding (first op of a micro-batch)
   __nv_bfloat16* dq; // [n, h]
   int64_t n, q_off, kv_len;
   int H, h;
@@ -999,9 +1000,18 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
         const float* tile = out + is_v * 128 * HD;
         const int col = (is_v ? p.h : 0) + head * HD;
 #pragma unroll
-        for (int b = 0; b < HD / 32; ++b) tc::tma_reduce_add_2d(&p.tdkv32, tile + b * 4096, col + 32 * b, static_cast<int>(j0));
-        if constexpr (HD % 32 == 16)
-          tc::tma_reduce_add_2d(&p.tdkv16, tile + (HD / 32) * 4096, col + HD - 16, static_cast<int>(j0));
+        for (int b = 0; b < HD / 32; ++b) {
+          if (p.dkv_store)
+            tc::tma_store_2d(&p.tdkv32, tile + b * 4096, col + 32 * b, static_cast<int>(j0));
+          else
+            tc::tma_reduce_add_2d(&p.tdkv32, tile + b * 4096, col + 32 * b, static_cast<int>(j0));
+        }
+        if constexpr (HD % 32 == 16) {
+          if (p.dkv_store)
+            tc::tma_store_2d(&p.tdkv16, tile + (HD / 32) * 4096, col + HD - 16, static_cast<int>(j0));
+          else
+            tc::tma_reduce_add_2d(&p.tdkv16, tile + (HD / 32) * 4096, col + HD - 16, static_cast<int>(j0));
+        }
       }
       tc::bulk_commit();
       tc::bulk_wait_read0();  // SMEM must outlive the copy-out
@@ -1726,7 +1736,7 @@ SideStream& side_stream() {
 }
 }  // namespace
 
-void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout, const float* lse, float* ws_delta,
+void attn_bwd_tc(bool dkv_overwrite, const void* q, const void* kv, const void* o, const void* dout, const float* lse, float* ws_delta,
                  float* ws_dq, void* dq, float* dkv, int64_t n, int64_t q_off, int64_t kv_len, int H, int hd,
                  cudaStream_t s) {
   const int h = H * hd;
@@ -1754,6 +1764,7 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
   a.ld = ws_delta;
   a.n_pad = n_pad;
   a.dkv = dkv;
+  a.dkv_store = dkv_overwrite ? 1 : 0;
   a.dq = static_cast<__nv_bfloat16*>(dq);
   {
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * h), static_cast<cuuint64_t>(kv_len)};
@@ -1808,6 +1819,7 @@ void attn_bwd_tc(const void* q, const void* kv, const void* o, const void* dout,
   }();
   if (hd == 80 && fused_env && ws_dq) {
     constexpr int HD = 80;
+    if (dkv_overwrite) SPK_CUDA(cudaMemsetAsync(dkv, 0, sizeof(float) * static_cast<size_t>(kv_len) * 2 * h, s));
     constexpr size_t smem = fused_smem_n<HD>(fused_stages<HD>());
     static_assert(smem <= 232448, "fused attention bwd smem");
     a.dqf = ws_dq;

@@ -586,7 +586,8 @@ void Stage::backward_impl(int m, int s, void* dx_target, const int32_t* tokens, 
   const int64_t n = sg.n, pos0 = sg.pos0, h = mc_.h, F = mc_.F, Fu = mc_.Fup;
   const DType dt = mc_.dt;
   const int attn_impl = (mc_.flags & SP_FLAG_NO_TC_ATTN) ? spk::kAttnSimt : spk::kAttnAuto;
-  if (s == k_) SPK_CUDA(cudaMemsetAsync(dkv_, 0, sizeof(float) * L_s_ * T_ * 2 * h, s_));
+  // s == k: the first backward op of the micro-batch covers every key row [0, T) and
+  // WRITES the dK/dV accumulator (attn_bwd dkv_overwrite) -- no memset, no zero read.
   const void* dy = sg.dy_in;
   for (int l = L_s_ - 1; l >= 0; --l) {
     const LayerW& w = lw_[l];
@@ -632,7 +633,7 @@ void Stage::backward_impl(int m, int s, void* dx_target, const int32_t* tokens, 
     const double attn_flops = 2.0 * 4.0 * h * (static_cast<double>(n) * pos0 + 0.5 * static_cast<double>(n) * n);
     if (probe && probe->enabled) probe->begin(KernelProbe::kAttnBwd, s_, attn_flops);
     spk::attn_bwd(dt, attn_impl, sg.q[l], kv(m, l), sg.o[l], w_t3_, sg.lse[l], w_delta_, w_dq_, w_t1_, dkv_l, n, pos0,
-                  pos0 + n, mc_.H, mc_.hd, s_);
+                  pos0 + n, mc_.H, mc_.hd, s_, /*dkv_overwrite=*/s == k_);
     if (probe && probe->enabled) probe->end(s_);
     flops += attn_flops;
     float* dkv_rows = dkv_l + pos0 * 2 * h;  // complete after this op (reverse causal order)
