@@ -268,6 +268,34 @@ __global__ void adamw_k(float* p, const float* __restrict__ g, float* m, float* 
   }
 }
 
+// 4 parameters per thread per step (float4 loads / stores; ~30 bytes of traffic
+// per parameter, HBM bound).
+template <typename T>
+__global__ void adamw_vec_k(float4* p, const float4* __restrict__ g, float4* m, float4* v, T* pc, int64_t n4, float lr,
+                            float b1, float b2, float eps, float wd, float bc1, float bc2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 gi = g[i];
+    float4 mi = m[i], vi = v[i], pi = p[i];
+    float* mf = &mi.x;
+    float* vf = &vi.x;
+    float* pf = &pi.x;
+    const float* gf = &gi.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      mf[e] = b1 * mf[e] + (1.f - b1) * gf[e];
+      vf[e] = b2 * vf[e] + (1.f - b2) * gf[e] * gf[e];
+      pf[e] -= lr * ((mf[e] / bc1) / (sqrtf(vf[e] / bc2) + eps) + wd * pf[e]);
+    }
+    m[i] = mi;
+    v[i] = vi;
+    p[i] = pi;
+    if (pc) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) pc[4 * i + e] = from_f<T>(pf[e]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ bf16 fast paths
 // Rows of h = 256*NV bf16: one warp per row, each lane owns NV chunks of 8
 // contiguous columns (16-byte loads/stores, fully coalesced), the row stays in
@@ -894,6 +922,14 @@ void fill_const(float* p, int64_t n, float v, cudaStream_t s) {
 void adamw(float* p, const float* g, float* m, float* v, void* pc, DType t, int64_t n, float lr, float b1, float b2,
            float eps, float wd, int step, cudaStream_t s) {
   const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
+  const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (n % 4 == 0 && al16(p) && al16(g) && al16(m) && al16(v)) {
+    SPK_DISPATCH(t, adamw_vec_k<T><<<stream_grid(n / 4, 256), 256, 0, s>>>(
+                        reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g), reinterpret_cast<float4*>(m),
+                        reinterpret_cast<float4*>(v), (T*)pc, n / 4, lr, b1, b2, eps, wd, bc1, bc2));
+    SPK_LAUNCH_CHECK();
+    return;
+  }
   SPK_DISPATCH(t, adamw_k<T><<<stream_grid(n, 256), 256, 0, s>>>(p, g, m, v, (T*)pc, n, lr, b1, b2, eps, wd, bc1, bc2));
   SPK_LAUNCH_CHECK();
 }

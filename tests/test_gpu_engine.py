@@ -208,3 +208,24 @@ def test_zero_bubble_input_weight_split(gpu, kind, k, dtype, tol):
     compare(eng, model, part, tok, rep, tol)
     eng.close()
 
+
+
+def test_adamw_update_matches_formula(gpu):
+    """One AdamW step (elementwise.cu adamw kernels) == the closed form at step 1:
+    m = (1-b1) g, v = (1-b2) g^2, p -= lr ((m/bc1) / (sqrt(v/bc2) + eps) + wd p)."""
+    model = tiny_model(dtype=E.BF16, layers=2, hidden=128, heads=2, ffn=256, vocab=256, max_seq=512)
+    model.lr, model.weight_decay = 1e-3, 0.1
+    cfg = scenario(model, P=2, M=3, k=2, T=512)
+    eng = E.Engine(cfg, "seq1f1b", pl.partition_for(cfg, "cwp"), model)
+    names = ["layer0.wqkv", "layer1.w2", "lm_head"] if "lm_head" in eng.params() else ["layer0.wqkv", "layer1.w2"]
+    before = {n: eng.read_param(n).astype(np.float64) for n in names}
+    eng.step(tokens_for(3, 512, 256))
+    b1, b2, eps = model.beta1, model.beta2, model.adam_eps
+    for n in names:
+        g = eng.read_grad(n).astype(np.float64)
+        p0 = before[n]
+        m, v = (1 - b1) * g, (1 - b2) * g * g
+        want = p0 - model.lr * ((m / (1 - b1)) / (np.sqrt(v / (1 - b2)) + eps) + model.weight_decay * p0)
+        got = eng.read_param(n).astype(np.float64)
+        assert np.max(np.abs(got - want)) < 1e-6, (n, np.max(np.abs(got - want)))
+    eng.close()
