@@ -232,10 +232,10 @@ __device__ __forceinline__ float2 ex2x2_sel(bool poly, float2 v) { return poly ?
 #define SPK_DKV_NS 3  // hd <= 80 dK/dV: score buffers (the dP^T buffers take the remaining 4 - NS)
 #endif
 #ifndef SPK_DQ_NS
-#define SPK_DQ_NS 3  // hd <= 80 dQ: score / dP buffers
+#define SPK_DQ_NS 3  // hd <= 80 dQ: score / dP buffers (3 + 2: -0.5 % bwd at sustained clocks vs 3 + 1)
 #endif
 #ifndef SPK_DQ_ND
-#define SPK_DQ_ND 1
+#define SPK_DQ_ND 2
 #endif
 #ifndef SPK_POLY_FWD
 #define SPK_POLY_FWD 2
