@@ -229,3 +229,20 @@ def test_adamw_update_matches_formula(gpu):
         got = eng.read_param(n).astype(np.float64)
         assert np.max(np.abs(got - want)) < 1e-6, (n, np.max(np.abs(got - want)))
     eng.close()
+
+
+@pytest.mark.parametrize("kind,k,mode", [("seq1f1b-i", 2, "cwp"), ("1f1b-i", 1, "even")])
+def test_interleaved_kinds_execute_reference_order(gpu, kind, k, mode):
+    """(f1) Seq1F1B-I / 1F1B-I: n_v = 2 stage chunks per device (V = 2P stages), executed
+    in-process in the reference's interleaved order (schedule.cpp:128-215); the executed log
+    is the reference generate() and the step matches the fp64 oracle (fp32 mode)."""
+    model = tiny_model(layers=4, hidden=128, heads=2, ffn=256, vocab=256, max_seq=512)
+    cfg = pl.ScenarioConfig(pipeline_size=2, stages_per_device=2, micro_batches=4, segments=k, seq_len=512,
+                            layers=model.layers, hidden_dim=model.hidden, param_count=model.param_count())
+    cfg.validate()
+    eng, part, tok, rep = run(model, cfg, kind=kind, mode=mode)
+    log = eng.op_log()
+    assert log.device_orders == ref.generate(cfg, kind, part).device_orders
+    assert ref.check_schedule(log) == []
+    compare(eng, model, part, tok, rep, TOL_F32)
+    eng.close()
