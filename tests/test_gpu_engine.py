@@ -246,3 +246,15 @@ def test_interleaved_kinds_execute_reference_order(gpu, kind, k, mode):
     assert ref.check_schedule(log) == []
     compare(eng, model, part, tok, rep, TOL_F32)
     eng.close()
+
+
+def test_bf16_gpt_2p7b_width_hd80(gpu):
+    """The production kernel mix at GPT-2.7B width (h 2560, 32 heads x 80, FFN 4h): tcgen05
+    attention at head dim 80 with the side-stream dQ kernel, the first-op dK/dV store, the
+    two-warp norm backward, vectorised CE, side-stream weight gradients -- one layer, bf16,
+    against the fp64 oracle."""
+    model = tiny_model(dtype=E.BF16, vocab=512, layers=1, hidden=2560, heads=32, ffn=4 * 2560, max_seq=512)
+    cfg = scenario(model, P=1, M=2, k=2, T=512)
+    eng, part, tok, rep = run(model, cfg)
+    compare(eng, model, part, tok, rep, TOL_BF16)
+    eng.close()
