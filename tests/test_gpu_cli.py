@@ -32,12 +32,15 @@ cost_model = flops
 """
 
 
-@pytest.mark.parametrize("kind,dtype", [("seq1f1b", "bf16"), ("seqzb1p", "f32")])
-def test_execute_writes_measured_report(tmp_path, gpu, kind, dtype):
+@pytest.mark.parametrize("kind,dtype,family", [("seq1f1b", "bf16", "gpt"), ("seqzb1p", "f32", "gpt"),
+                                               ("seq1f1b", "bf16", "llama")])
+def test_execute_writes_measured_report(tmp_path, gpu, kind, dtype, family):
     cfgf = tmp_path / "tiny.cfg"
     cfgf.write_text(TINY)
+    heads = "4" if family == "gpt" else "2"
     r = subprocess.run([str(CLI), "execute", "--config", str(cfgf), "--kind", kind, "--partition", "cwp",
-                        "--heads", "4", "--vocab", "512", "--ffn", "1024", "--dtype", dtype, "--steps", "2",
+                        "--family", family, "--heads", heads, "--vocab", "512", "--ffn", "1024", "--dtype", dtype,
+                        "--steps", "2",
                         "--out", str(tmp_path / "rep.json"), "--gantt", "ascii", "--gantt-width", "80", "--summary"],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr
