@@ -236,7 +236,7 @@ typedef struct sp_comm_op {
   int32_t when;       /* 0: before the op (receive), 1: after the op (send)           */
   int32_t dir;        /* SP_COMM_SEND / SP_COMM_RECV                                  */
   int32_t peer;       /* peer rank (device - 1)                                       */
-  int32_t channel;    /* 0/1 activations (even/odd edge), 2/3 gradients               */
+  int32_t channel;    /* pipeline edge (v, v+1): 2(v-1) activations, 2(v-1)+1 gradients */
   int32_t kind;       /* task kind of the op                                          */
   int32_t micro_batch, segment, stage;
   int32_t reserved;
@@ -318,10 +318,24 @@ int sp_engine_destroy(sp_engine* eng);
  * dK/dV accumulator. Used to report configurations that would not fit (e.g. 1F1B at 128K). */
 int sp_plan_memory(const sp_scenario* cfg, int32_t schedule_kind, const int64_t* lengths, const sp_model* model,
                    int32_t stage, double* live_peak_bytes, double* arena_bytes, double* dkv_bytes);
-/* NCCL bootstrap: rank 0 calls sp_nccl_unique_id, the id bytes travel by any side channel,
- * every rank calls sp_engine_comm_init. */
+/* Multi-rank data plane (world_size == pipeline_size). One channel per pipeline edge and direction
+ * (sp_comm_op.channel); sp_engine_comm_channels gives their number.
+ * NCCL (one process per GPU): rank 0 calls sp_nccl_unique_id once per channel, the id bytes travel by
+ * any side channel, every rank calls sp_engine_comm_init with all of them (one communicator each).
+ * In-process (several engines in one process, one host thread each, e.g. P ranks on one GPU):
+ * sp_local_hub_create once, sp_engine_attach_local on every engine; a receive that does not pair up
+ * within watchdog_seconds fails with SP_ERR_DEADLOCK instead of hanging. */
+typedef struct sp_local_hub sp_local_hub;
+int sp_engine_comm_channels(sp_engine* eng, int32_t* n);
 int sp_nccl_unique_id(uint8_t* out, size_t len);
 int sp_engine_comm_init(sp_engine* eng, const uint8_t* const* ids, int32_t n_ids);
+int sp_local_hub_create(int32_t world_size, double watchdog_seconds, sp_local_hub** out);
+int sp_local_hub_destroy(sp_local_hub* hub);
+int sp_engine_attach_local(sp_engine* eng, sp_local_hub* hub);
+/* Single-rank engines: capture the step body (every op of the op table + the optimizer) into a
+ * CUDA graph on the next step and replay it from then on (on != 0); 0 returns to eager launches.
+ * Steps with SP_FLAG_KPROBE run eagerly. */
+int sp_engine_enable_graph(sp_engine* eng, int32_t on);
 /* Replace the engine's SP_FLAG_* set (e.g. turn kernel probes on for a timed region). */
 int sp_engine_set_flags(sp_engine* eng, int32_t flags);
 /* tokens: micro_batches x (seq_len + 1) int32 (inputs are [:, :T], labels [:, 1:]).

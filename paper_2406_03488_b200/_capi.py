@@ -127,6 +127,11 @@ _SIGS = {
                                  P(C.c_double), P(C.c_double)]),
     "sp_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_size_t]),
     "sp_engine_comm_init": (C.c_int, [C.c_void_p, P(C.c_char_p), C.c_int32]),
+    "sp_engine_comm_channels": (C.c_int, [C.c_void_p, P(C.c_int32)]),
+    "sp_local_hub_create": (C.c_int, [C.c_int32, C.c_double, P(C.c_void_p)]),
+    "sp_local_hub_destroy": (C.c_int, [C.c_void_p]),
+    "sp_engine_attach_local": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sp_engine_enable_graph": (C.c_int, [C.c_void_p, C.c_int32]),
     "sp_engine_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, P(StepReport)]),
     "sp_engine_set_flags": (C.c_int, [C.c_void_p, C.c_int32]),
     "sp_engine_op_log": (C.c_int, [C.c_void_p, P(Task), P(C.c_int64)]),
@@ -186,11 +191,11 @@ def lib():
         if not LIB_PATH.exists():
             raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2406_03488_b200.build` "
                                "(no CPU/Python fallback exists)")
-        path = LIB_PATH
-        variant = os.environ.get("SP_LIB_VARIANT")  # kernel-tuning builds (tools/build_variant.py)
-        if variant:
-            path = LIB_PATH.parent / "variants" / f"libseqpipe_b200_{variant}.so"
-        _lib = C.CDLL(str(path))
+        for var in ("SP_LIB_VARIANT", "SP_ATTN_DBG", "SP_ATTN_TRACE"):
+            if os.environ.get(var):  # profiling-only knobs of earlier tuning builds: refuse, never honour
+                raise RuntimeError(f"{var} is set: the product library has no debug / variant switches "
+                                   "(profiling builds live under tools/); unset it")
+        _lib = C.CDLL(str(LIB_PATH))
         for name, (res, args) in _SIGS.items():
             fn = getattr(_lib, name, None)
             if fn is None:

@@ -16,6 +16,10 @@ struct sp_engine {
   std::unique_ptr<spe::Engine> impl;
 };
 
+struct sp_local_hub {
+  std::shared_ptr<spe::LocalHub> impl;
+};
+
 namespace {
 
 template <typename F>
@@ -144,6 +148,35 @@ int sp_engine_comm_init(sp_engine* eng, const uint8_t* const* ids, int32_t n_ids
     for (int i = 0; i < n_ids; ++i) v.emplace_back(reinterpret_cast<const char*>(ids[i]), sizeof(ncclUniqueId));
     E(eng).comm_init(v);
   });
+}
+
+int sp_engine_comm_channels(sp_engine* eng, int32_t* n) {
+  return eguard([&] { *n = E(eng).comm_channels(); });
+}
+
+int sp_local_hub_create(int32_t world_size, double watchdog_seconds, sp_local_hub** out) {
+  return eguard([&] {
+    if (!out) throw std::invalid_argument("null output");
+    auto h = std::make_unique<sp_local_hub>();
+    h->impl = spe::make_local_hub(world_size, watchdog_seconds > 0 ? watchdog_seconds : 600.0);
+    *out = h.release();
+  });
+}
+
+int sp_local_hub_destroy(sp_local_hub* hub) {
+  delete hub;
+  return SP_OK;
+}
+
+int sp_engine_attach_local(sp_engine* eng, sp_local_hub* hub) {
+  return eguard([&] {
+    if (!hub || !hub->impl) throw std::invalid_argument("null hub");
+    E(eng).attach_local(hub->impl);
+  });
+}
+
+int sp_engine_enable_graph(sp_engine* eng, int32_t on) {
+  return eguard([&] { E(eng).enable_graph(on != 0); });
 }
 
 int sp_engine_set_flags(sp_engine* eng, int32_t flags) {

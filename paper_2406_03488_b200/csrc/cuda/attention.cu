@@ -1,5 +1,7 @@
 // Attention dispatch: fp32 validation mode -> SIMT kernels; bf16 production
-// mode -> tensor-core kernels (attention_tc.cu) when the head dim is supported.
+// mode -> tensor-core kernels (attention_tc.cu), head dim 64 / 80 / 128. A bf16
+// call the tensor-core kernels cannot take is an error (no silent SIMT fallback);
+// SIMT in bf16 only on an explicit request (kAttnSimt: SP_FLAG_NO_TC_ATTN, tests).
 #include "cuda/common.cuh"
 #include "cuda/ops.h"
 
@@ -21,8 +23,10 @@ void attn_fwd(DType t, int impl, const void* q, const void* kv, void* o, float* 
               int64_t kv_len, int H, int hd, cudaStream_t s) {
   if (n == 0) return;
   if (kv_len != q_off + n) throw std::invalid_argument("attention: kv_len must equal q_off + n (causal prefix)");
-  const bool tc = impl != kAttnSimt && attn_tc_supported(t, hd);
-  if (impl == kAttnTensor && !tc) throw std::invalid_argument("attention: tensor-core path unsupported for this dtype/head_dim");
+  const bool tc = impl != kAttnSimt && t == DType::kBF16;
+  if (impl == kAttnTensor && t != DType::kBF16) throw std::invalid_argument("attention: tensor-core path needs bf16");
+  if (tc && !attn_tc_supported(t, hd))
+    throw std::invalid_argument("attention: bf16 tensor-core kernels support head_dim 64, 80, 128 (no SIMT fallback)");
   if (tc)
     attn_fwd_tc(q, kv, o, lse, n, q_off, kv_len, H, hd, s);
   else
@@ -34,8 +38,10 @@ void attn_bwd(DType t, int impl, const void* q, const void* kv, const void* o, c
               cudaStream_t s, bool dkv_overwrite) {
   if (n == 0) return;
   if (kv_len != q_off + n) throw std::invalid_argument("attention: kv_len must equal q_off + n (causal prefix)");
-  const bool tc = impl != kAttnSimt && attn_tc_supported(t, hd);
-  if (impl == kAttnTensor && !tc) throw std::invalid_argument("attention: tensor-core path unsupported for this dtype/head_dim");
+  const bool tc = impl != kAttnSimt && t == DType::kBF16;
+  if (impl == kAttnTensor && t != DType::kBF16) throw std::invalid_argument("attention: tensor-core path needs bf16");
+  if (tc && !attn_tc_supported(t, hd))
+    throw std::invalid_argument("attention: bf16 tensor-core kernels support head_dim 64, 80, 128 (no SIMT fallback)");
   if (tc) {
     attn_bwd_tc(dkv_overwrite, q, kv, o, dout, lse, ws_delta, ws_dq, dq, dkv, n, q_off, kv_len, H, hd, s);
   } else {

@@ -40,14 +40,11 @@ namespace {
 
 constexpr int BQ = 128, BKV = 128;
 
-#ifndef SPK_ATTN_NARROW80
-#define SPK_ATTN_NARROW80 0  // hd 80 as 64 + 16 columns (SW128 + SW32): measured slower (N=16 MMAs, 32-byte TMA rows)
-#endif
-
 template <int HD>
 struct Lay {
-  static constexpr bool NARROW = HD == 80 && SPK_ATTN_NARROW80;  // hd 80: SW32 16-column second chunk
-  static constexpr int C1 = HD <= 64 ? 0 : (NARROW ? 16 : 64);  // columns held by the second chunk
+  // hd 80 holds its last 16 columns in a second 64-wide SW128 chunk (padded): one N = hd MMA per
+  // K step. (A 64 + 16 SW32 split measured slower: N = 16 MMAs and 32-byte TMA rows.)
+  static constexpr int C1 = HD <= 64 ? 0 : 64;  // columns held by the second chunk
   static constexpr int R1 = C1 * 2;                              // bytes per row of the second chunk
   static constexpr int bytes(int rows) { return rows * (128 + R1); }
 };
@@ -56,37 +53,21 @@ struct Lay {
 template <int HD>
 __device__ __forceinline__ uint64_t kdesc(uint32_t base, int rows, int kk) {
   if (kk < 4) return tc::smem_desc(base + kk * 32, 16, 1024, tc::kSwizzle128B);
-  if constexpr (Lay<HD>::NARROW) {
-    return tc::smem_desc(base + rows * 128, 16, 256, tc::kSwizzle32B);
-  } else {
-    return tc::smem_desc(base + rows * 128 + (kk - 4) * 32, 16, 1024, tc::kSwizzle128B);
-  }
+  return tc::smem_desc(base + rows * 128 + (kk - 4) * 32, 16, 1024, tc::kSwizzle128B);
 }
 
 // D[128 x hd] (+)= A[128 x 16 (K step kk)] * B[K rows of a [rows x hd] tile]^T, B MN-major.
 template <int HD>
 __device__ __forceinline__ void mma_nhd(uint32_t d, uint64_t adesc, uint32_t bbase, int rows, int kk, bool acc) {
-  if constexpr (Lay<HD>::NARROW) {
-    constexpr uint32_t i64 = tc::idesc_bf16(128, 64, false, true), i16 = tc::idesc_bf16(128, 16, false, true);
-    tc::mma_bf16_ss_w(d, adesc, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), i64, acc);
-    tc::mma_bf16_ss_w(d + 64, adesc, tc::smem_desc(bbase + rows * 128 + kk * 512, 256, 256, tc::kSwizzle32B), i16, acc);
-  } else {  // padded second chunk: one N = hd MMA
-    constexpr uint32_t id = tc::idesc_bf16(128, HD, false, true);
-    tc::mma_bf16_ss_w(d, adesc, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), id, acc);
-  }
+  constexpr uint32_t id = tc::idesc_bf16(128, HD, false, true);  // padded second chunk: one N = hd MMA
+  tc::mma_bf16_ss_w(d, adesc, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), id, acc);
 }
 
 // Same with A (M=128 x K=16, bf16 packed two per 32-bit column) read from TMEM.
 template <int HD>
 __device__ __forceinline__ void mma_nhd_ts(uint32_t d, uint32_t a_tmem, uint32_t bbase, int rows, int kk, bool acc) {
-  if constexpr (Lay<HD>::NARROW) {
-    constexpr uint32_t i64 = tc::idesc_bf16(128, 64, false, true), i16 = tc::idesc_bf16(128, 16, false, true);
-    tc::mma_bf16_ts_w(d, a_tmem, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), i64, acc);
-    tc::mma_bf16_ts_w(d + 64, a_tmem, tc::smem_desc(bbase + rows * 128 + kk * 512, 256, 256, tc::kSwizzle32B), i16, acc);
-  } else {
-    constexpr uint32_t id = tc::idesc_bf16(128, HD, false, true);
-    tc::mma_bf16_ts_w(d, a_tmem, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), id, acc);
-  }
+  constexpr uint32_t id = tc::idesc_bf16(128, HD, false, true);
+  tc::mma_bf16_ts_w(d, a_tmem, tc::smem_desc(bbase + kk * 2048, rows * 128, 1024, tc::kSwizzle128B), id, acc);
 }
 
 
@@ -225,9 +206,6 @@ __device__ __forceinline__ float2 ex2x2_poly(float2 x) {
 // `poly` is a constant after the softmax loops are unrolled.
 __device__ __forceinline__ float2 ex2x2_sel(bool poly, float2 v) { return poly ? ex2x2_poly(v) : ex2x2(v); }
 // Which groups of a fully unrolled softmax loop use the FMA-pipe exponential: 3 of 8.
-#ifndef SPK_FWD_TURN
-#define SPK_FWD_TURN 0  // measured slower at hd 80 (variant sweep); forward tiles alternate their exponentials: 0 off, 1 before exp, 2 whole block
-#endif
 #ifndef SPK_DKV_NS
 #define SPK_DKV_NS 3  // hd <= 80 dK/dV: score buffers (the dP^T buffers take the remaining 4 - NS)
 #endif
@@ -334,7 +312,6 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
   uint64_t* s_full = bars + 1;   // [2 tiles]
   uint64_t* p_full = bars + 3;   // [2 tiles]  P packed into the tile's S buffer
   uint64_t* pv_done = bars + 5;  // [2 tiles]  O += P V completed
-  uint64_t* turn = bars + 7;     // [2 tiles]  tile t finished the exponentials of a block
   uint64_t* k_full = bars + 16;          // [KVS]
   uint64_t* k_empty = k_full + KVS;      // [KVS]
   uint64_t* v_full = k_empty + KVS;      // [KVS]
@@ -368,7 +345,6 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
       tc::mbar_init(&s_full[t], 1);
       tc::mbar_init(&p_full[t], 8);  // the tile's softmax warps
       tc::mbar_init(&pv_done[t], 1);
-      tc::mbar_init(&turn[t], 8);
     }
     for (int i = 0; i < KVS; ++i) {
       tc::mbar_init(&k_full[i], 1);
@@ -489,8 +465,6 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
       const int64_t lim64 =
           (valid ? (qpos < p.kv_len - 1 ? qpos : p.kv_len - 1) : -1) - static_cast<int64_t>(j) * BKV - 64 * hf;
       const int lim = lim64 > 1000000 ? 1000000 : static_cast<int>(lim64);  // local columns <= lim are visible
-      if (SPK_FWD_TURN == 2 && (t == 0 ? (j > 0 && j - 1 < nblk_t[1]) : (j < nblk_t[0])))
-        tc::mbar_wait(&turn[t ^ 1], t == 0 ? ((j - 1) & 1) : (j & 1));
       tc::mbar_wait(&s_full[t], j & 1);
       tc::tc_fence_after();
       const uint32_t sbase = tmem + lane_base + t * 128 + 64 * hf;
@@ -543,13 +517,6 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
         l *= alpha;
         m = m_new;
       }
-      // The two tiles take turns on the exponentials (A(j), B(j), A(j+1), ...):
-      // the MUFU / issue slots then serve one tile at a time while the tensor pipe
-      // runs the other tile's PV and next S, instead of both softmaxes sharing the
-      // SM and finishing together. turn[u] cannot run two phases ahead of the
-      // waiter: each side waits for the other before its next block.
-      if (SPK_FWD_TURN == 1 && (t == 0 ? (j > 0 && j - 1 < nblk_t[1]) : (j < nblk_t[0])))
-        tc::mbar_wait(&turn[t ^ 1], t == 0 ? ((j - 1) & 1) : (j & 1));
       const float neg_m = m == -INFINITY ? 0.f : -m;
       const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(neg_m, neg_m);
       float2 rs_a = make_float2(0.f, 0.f), rs_b = make_float2(0.f, 0.f);
@@ -572,7 +539,6 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
       tc::tmem_st_wait();
       tc::tc_fence_before();
       warp_arrive(&p_full[t]);
-      if (SPK_FWD_TURN) warp_arrive(&turn[t]);
     }
     if (nb > 0) {
       {  // combine the two halves' partial row sums
@@ -612,12 +578,16 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_tc_k(const __grid_constant__ 
 
 // ============================================================================ backward
 
+// Profiling hooks (skip MMAs / softmax, cycle-stamp one CTA) exist only in builds made with
+// -DSPK_ATTN_PROFILING=1 (tools/); release builds compile them out and read no environment.
+#ifndef SPK_ATTN_PROFILING
+#define SPK_ATTN_PROFILING 0
+#endif
+
 struct __align__(64) AttnBwdParams {
   CUtensorMap tdkv;  // dkv fp32 [kv_len, 2h], [128 x HD] boxes (TMA reduce-add of dK / dV)
   CUtensorMap tdkv32;  // the same tensor, [128 x 32] boxes, 128-byte swizzle (swizzled dK/dV staging)
   CUtensorMap tdkv16;  // [128 x 16] boxes, 64-byte swizzle (the last 16 columns of head dim 80)
-  CUtensorMap tdq;   // dQ fp32 [n, h], [128 x 32] boxes, 128-byte swizzle (fused kernel: TMA reduce-add)
-  CUtensorMap tdq16; // the same, [128 x 16] boxes, 64-byte swizzle (head-dim columns 64..79)
   Maps tq;           // q  [n, h]
   Maps tdo;          // dO [n, h]
   Maps tkv;          // kv [kv_len, 2h]
@@ -625,16 +595,13 @@ struct __align__(64) AttnBwdParams {
   const float* ld;   // [H][n_pad / 64][-LSE*log2e x 64, -delta x 64], zero padded (attn_prep_k)
   int64_t n_pad;     // n rounded up to 128
   float* dkv;        // [kv_len, 2h] fp32 accumulator
-  float* dqf;        // [n, h] fp32 dQ accumulator (fused kernel; zeroed by the host)
   int dkv_store;     // dK/dV epilogue writes (TMA store) instead of adding (first op of a micro-batch)
   __nv_bfloat16* dq; // [n, h]
   int64_t n, q_off, kv_len;
   int H, h;
   float scale, scale_log2;
-  int dbg;  // profiling only (SP_ATTN_DBG): 1 = skip dK/dV MMAs, 2 = skip the dK/dV softmax (TMEM ld/st + math);
-            // fused kernel: 16 = skip the dQ reduce, 32 = skip the dQ MMAs, 64 = skip the dS^T staging,
-            // 128 = skip its proxy fence
-  unsigned long long* trace;  // profiling only (SP_ATTN_TRACE): cycle stamps of one CTA, [event][iteration]
+  int dbg;  // profiling builds only (SPK_ATTN_PROFILING): 1 = skip dK/dV MMAs, 2 = skip the dK/dV softmax
+  unsigned long long* trace;  // profiling builds only: cycle stamps of one CTA, [event][iteration]
 };
 
 // ---------------------------------------------------------------- backward layout
@@ -686,6 +653,8 @@ template <int HD>
 constexpr size_t dq_smem_n(int st) {
   return 2 * st * Lay<HD>::bytes(64) + (20 + 2 * st) * 8 + 8 + 1024;
 }
+__device__ __forceinline__ int prof_dbg(const AttnBwdParams& p) { return SPK_ATTN_PROFILING ? p.dbg : 0; }
+
 template <int HD>
 constexpr int dq_stages() {
   int st = 8;
@@ -700,6 +669,7 @@ constexpr size_t dq_smem() {
 // Debug timeline (SP_ATTN_TRACE=1): clock64 stamps of the last CTA of head 0,
 // 16 events x 64 iterations; printed by the host after the launch.
 __device__ __forceinline__ void trace_mark(const AttnBwdParams& p, int ev, int it) {
+  if constexpr (!SPK_ATTN_PROFILING) return;
   // every lane stores the same stamp: no lane-divergent branch in the MMA warp
   if (p.trace && it < 64 && blockIdx.x == gridDim.x - 1 && blockIdx.y == 0) p.trace[ev * 64 + it] = clock64();
 }
@@ -826,7 +796,7 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
       const int st = it % QST;
       tc::mbar_wait_w(&q_full[st], (it / QST) & 1);
       tc::tc_fence_after();
-      if (!(p.dbg & 1)) kv_mma(tmem + (it % NS) * 64, C::T_K, k_base, tc::smem_u32(sQ + st * Q_T));
+      if (!(prof_dbg(p) & 1)) kv_mma(tmem + (it % NS) * 64, C::T_K, k_base, tc::smem_u32(sQ + st * Q_T));
       tc::mma_commit_w(&s_full[it % NS]);
       trace_mark(p, 3, it);
     };
@@ -839,7 +809,7 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
         tc::mbar_wait_w(&q_full[st], (it / QST) & 1);
         if (it >= ND) tc::mbar_wait_w(&dp_free[it % ND], ((it / ND) - 1) & 1);
         tc::tc_fence_after();
-        if (!(p.dbg & 1)) kv_mma(tmem + C::T_DP + (it % ND) * 64, C::T_V, v_base, tc::smem_u32(sdO + st * Q_T));
+        if (!(prof_dbg(p) & 1)) kv_mma(tmem + C::T_DP + (it % ND) * 64, C::T_V, v_base, tc::smem_u32(sdO + st * Q_T));
         tc::mma_commit_w(&dp_full[it % ND]);
         trace_mark(p, 2, it);
       }
@@ -854,7 +824,7 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
         tc::mbar_wait_w(&sm_done[b], (it / NS) & 1);
         tc::tc_fence_after();
         const uint32_t q_base = tc::smem_u32(sQ + st * Q_T), do_base = tc::smem_u32(sdO + st * Q_T);
-        if (!(p.dbg & 1)) {
+        if (!(prof_dbg(p) & 1)) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries
             const bool acc = it > 0 || kk > 0;
@@ -905,7 +875,7 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
       uint32_t sv[16], dpv[16];
       tc::mbar_wait(&s_full[b], (it / NS) & 1);
       if (warp == 4) trace_mark(p, 5, it);
-      if (p.dbg & 2) {  // protocol only
+      if (prof_dbg(p) & 2) {  // protocol only
         tc::mbar_wait(&dp_full[d], (it / ND) & 1);
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&dp_free[d]);
@@ -1230,392 +1200,6 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dq_k(const __grid_constant__ 
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-// ---------------------------------------------------------------- fused dK/dV/dQ (head dim 80)
-// The dK/dV kernel above plus dQ, so the backward no longer recomputes S and dP in a
-// separate dQ kernel (2 of its 7 GEMM-equivalents and one exp pass). K and V arrive
-// once per CTA by TMA: K stays in SMEM (A of S^T = K Q^T, SS form; B of dQ, MN-major),
-// V is copied into TMEM (A of dP^T, TS form). Each softmax thread also writes its 16
-// dS^T values (one key row) into an SMEM tile laid out as the MN-major A operand of
-// dQ = dS K; after every second 64-query block one M = 128 (two blocks of queries)
-// x N = 80 x K = 128 keys MMA group accumulates dQ in TMEM, which the softmax warps
-// drain one pair later with red.global.add.v4.f32 into an fp32 [n, h] workspace
-// (summed over the key tiles; the host scales and casts it into dq).
-// TMEM: S^T [2] x 64 | dP^T 64 | dV 80 | dQ 80 | dK 80 | K 40 | V 40 (bf16 pairs).
-struct FusedCfg {
-  static constexpr int NS = 2, ND = 1;
-  static constexpr uint32_t T_DP = 128, T_DV = 192, T_DQ = 272, T_DK = 352, T_K = 432, T_V = 472;
-};
-constexpr int FUSED_DS_T = 2 * 128 * 128;  // one dS^T tile: 2 query halves x 128 keys x 128 B
-template <int HD>
-constexpr size_t fused_smem_n(int st) {
-  return static_cast<size_t>(2 * Lay<HD>::bytes(128) + FUSED_DS_T + 128 * HD * 4) + 2 * st * Lay<HD>::bytes(64) +
-         st * 512 + (24 + 2 * st) * 8 + 8 + 1024;
-}
-template <int HD>
-constexpr int fused_stages() {
-  int st = 8;
-  while (fused_smem_n<HD>(st) > 232448) --st;
-  return st;
-}
-
-// Half `part` of row r of a TMA-staged [rows x hd] tile (Lay<HD> chunks, 128 B swizzle)
-// -> HD / 4 32-bit TMEM columns at taddr.
-template <int HD>
-__device__ __forceinline__ void row_part_smem_to_tmem(uint32_t taddr, const uint8_t* tile, int rows, int r, int part) {
-  constexpr int NU = HD / 16;  // 16-byte units per half row
-  uint32_t v[HD / 4];
-#pragma unroll
-  for (int i = 0; i < NU; ++i) {
-    const int c8 = part * NU + i, chunk = c8 >> 3, u = c8 & 7;
-    const uint4 x = *reinterpret_cast<const uint4*>(tile + chunk * rows * 128 + r * 128 + ((u ^ (r & 7)) << 4));
-    v[4 * i] = x.x;
-    v[4 * i + 1] = x.y;
-    v[4 * i + 2] = x.z;
-    v[4 * i + 3] = x.w;
-  }
-  constexpr int NC = HD / 4;
-#pragma unroll
-  for (int c = 0; c + 8 <= NC; c += 8) tc::tmem_st8(taddr + c, v + c);
-  if constexpr (NC % 8 == 4) tc::tmem_st4(taddr + NC - 4, v + NC - 4);
-}
-
-template <int HD>
-__global__ void __launch_bounds__(640, 1) attn_bwd_fused_k(const __grid_constant__ AttnBwdParams p) {
-  static_assert(HD == 80, "fused dK/dV/dQ kernel: head dim 80");
-  using C = FusedCfg;
-  constexpr int QST = fused_stages<HD>();
-  constexpr int NS = C::NS;
-  constexpr int KV_T = Lay<HD>::bytes(128), Q_T = Lay<HD>::bytes(64);
-  static_assert(2 * 128 * HD * 4 <= 2 * KV_T + FUSED_DS_T + QST * 2 * Q_T, "dK/dV epilogue staging");
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sK = sm;
-  uint8_t* sV = sK + KV_T;           // V tile; dS^T buffer 0 once V is in TMEM
-  uint8_t* sDS1 = sV + KV_T;         // dS^T buffer 1
-  float* sDQ = reinterpret_cast<float*>(sDS1 + FUSED_DS_T);  // [128 queries][HD] fp32 dQ staging
-  uint8_t* sQ = reinterpret_cast<uint8_t*>(sDQ + 128 * HD);  // [QST]
-  uint8_t* sdO = sQ + QST * Q_T;     // [QST]
-  float* sLD = reinterpret_cast<float*>(sdO + QST * Q_T);  // [QST][-LSE*log2e x 64, -delta x 64]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + QST * 128);
-  uint64_t* kv_full = bars;        // K / V tiles landed (TMA)
-  uint64_t* v_tmem = bars + 1;     // V copied into TMEM (16 softmax warps)
-  uint64_t* done = bars + 2;
-  uint64_t* s_full = bars + 3;     // [2]
-  uint64_t* sm_done = bars + 5;    // [2]  P^T / dS^T packed (TMEM) and dS^T staged (SMEM)
-  uint64_t* dp_full = bars + 7;
-  uint64_t* dp_free = bars + 8;
-  uint64_t* dq_full = bars + 9;    // [2]  dQ of query-block pair q (parity q & 1) accumulated
-  uint64_t* dq_free = bars + 11;   // dQ accumulator drained
-  uint64_t* q_full = bars + 12;          // [QST]
-  uint64_t* q_empty = q_full + QST;      // [QST]
-  uint64_t* s_free = q_empty + QST;      // [2]
-  uint64_t* stage_full = s_free + NS;    // dQ staging tile written (16 softmax warps)
-  uint64_t* stage_free = stage_full + 1; // the reduce of the tile has read it (warp 4, lane 0)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stage_free + 1);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = tc::cluster_ctarank();
-  const int num_kb = static_cast<int>((p.kv_len + 127) / 128);
-  const int num_kb2 = (num_kb + 1) & ~1;
-  const int kb = num_kb2 - 1 - static_cast<int>(blockIdx.x);
-  const int head = blockIdx.y;
-  const int64_t j0 = static_cast<int64_t>(kb) * 128;
-  const int64_t j0_lo = static_cast<int64_t>(num_kb2 - 2 - 2 * static_cast<int>(blockIdx.x / 2)) * 128;
-  int64_t ib0 = j0_lo - p.q_off;
-  if (ib0 < 0) ib0 = 0;
-  ib0 = ib0 / 128 * 128;  // dQ pairs two 64-query blocks
-  const int niter = static_cast<int>((p.n - ib0 + 127) / 128) * 2;
-  const int npair = niter / 2;
-
-  if (threadIdx.x == 0) {
-    tc::mbar_init(kv_full, 1);
-    tc::mbar_init(v_tmem, 16);
-    tc::mbar_init(done, 1);
-    for (int i = 0; i < NS; ++i) {
-      tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&sm_done[i], 16);
-      tc::mbar_init(&s_free[i], 1);
-      tc::mbar_init(&dq_full[i], 1);
-    }
-    tc::mbar_init(dp_full, 1);
-    tc::mbar_init(dp_free, 16);
-    tc::mbar_init(dq_free, 16);
-    tc::mbar_init(stage_full, 16);
-    tc::mbar_init(stage_free, 1);
-    for (int i = 0; i < QST; ++i) {
-      tc::mbar_init(&q_full[i], 1);
-      tc::mbar_init(&q_empty[i], 2);
-    }
-    tc::fence_mbar_init();
-  }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
-  tc::tc_fence_before();
-  tc::cluster_sync();
-  tc::tc_fence_after();
-  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-
-  if (warp == 0) {
-    if (lane == 0) {
-      tc::tma_prefetch(&p.tq.m0);
-      tc::tma_prefetch(&p.tdo.m0);
-      tc::tma_prefetch(&p.tkv.m0);
-      tc::mbar_expect_tx(kv_full, 2 * KV_T);
-      load_tile<HD>(sK, p.tkv, kv_full, head * HD, static_cast<int>(j0), 128, 0);
-      load_tile<HD>(sV, p.tkv, kv_full, p.h + head * HD, static_cast<int>(j0), 128, 0);
-      for (int it = 0; it < niter; ++it) {
-        const int st = it % QST;
-        const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
-        tc::mbar_wait(&q_empty[st], ((it / QST) & 1) ^ 1);
-        tc::mbar_expect_tx(&q_full[st], 2 * Q_T + 512);
-        if (rank == 0)
-          load_tile<HD>(sQ + st * Q_T, p.tq, &q_full[st], head * HD, static_cast<int>(i0), 64, 3);
-        else
-          load_tile<HD>(sdO + st * Q_T, p.tdo, &q_full[st], head * HD, static_cast<int>(i0), 64, 3);
-        tc::bulk_load(sLD + st * 128, p.ld + (static_cast<int64_t>(head) * p.n_pad + i0) * 2, 512, &q_full[st]);
-      }
-    }
-  } else if (warp >= 1 && warp <= 3) {
-    constexpr uint32_t idesc_s = tc::idesc_bf16(128, 64, false, false);
-    const uint32_t k_base = tc::smem_u32(sK);
-    tc::mbar_wait_w(kv_full, 0);
-    tc::tc_fence_after();
-    if (warp == 1) {  // dP^T = V dO^T (A = V in TMEM)
-      tc::mbar_wait_w(v_tmem, 0);
-      tc::tc_fence_after();
-      for (int it = 0; it < niter; ++it) {
-        const int st = it % QST;
-        tc::mbar_wait_w(&q_full[st], (it / QST) & 1);
-        if (it >= 1) tc::mbar_wait_w(dp_free, (it - 1) & 1);
-        tc::tc_fence_after();
-        const uint32_t do_base = tc::smem_u32(sdO + st * Q_T);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          tc::mma_bf16_ts_w(tmem + C::T_DP, tmem + C::T_V + 8 * kk, kdesc<HD>(do_base, 64, kk), idesc_s, kk > 0);
-        tc::mma_commit_w(dp_full);
-      }
-    } else if (warp == 3) {  // S^T = K Q^T (A = K copied into TMEM)
-      tc::mbar_wait_w(v_tmem, 0);
-      tc::tc_fence_after();
-      for (int it = 0; it < niter; ++it) {
-        const int st = it % QST;
-        if (it >= NS) tc::mbar_wait_w(&s_free[it % NS], ((it / NS) - 1) & 1);
-        tc::mbar_wait_w(&q_full[st], (it / QST) & 1);
-        tc::tc_fence_after();
-        const uint32_t q_base = tc::smem_u32(sQ + st * Q_T);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          tc::mma_bf16_ts_w(tmem + (it % NS) * 64, tmem + C::T_K + 8 * kk, kdesc<HD>(q_base, 64, kk), idesc_s, kk > 0);
-        tc::mma_commit_w(&s_full[it % NS]);
-      }
-    } else {  // dV += P^T dO, dK += dS^T Q; after each odd block: dQ(pair) = dS K
-      constexpr uint32_t idesc_q = tc::idesc_bf16(128, HD, true, true);
-      for (int it = 0; it < niter; ++it) {
-        const int b = it % NS, st = it % QST;
-        tc::mbar_wait_w(&sm_done[b], (it / NS) & 1);
-        tc::tc_fence_after();
-        const uint32_t q_base = tc::smem_u32(sQ + st * Q_T), do_base = tc::smem_u32(sdO + st * Q_T);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const bool acc = it > 0 || kk > 0;
-          const uint32_t col = b * 64 + 16 * kk;
-          mma_nhd_ts<HD>(tmem + C::T_DV, tmem + col, do_base, 64, kk, acc);
-          mma_nhd_ts<HD>(tmem + C::T_DK, tmem + col + 8, q_base, 64, kk, acc);
-        }
-        tc::mma_commit_mc_w(&q_empty[st], 3);
-        tc::mma_commit_w(&s_free[b]);
-        if (it & 1) {
-          const int q = it >> 1;
-          if (q >= 1) tc::mbar_wait_w(dq_free, (q - 1) & 1);  // pair q-1 drained from TMEM
-          tc::tc_fence_after();
-          const uint32_t ds_base = tc::smem_u32((q & 1) ? sDS1 : sV);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)  // K = 128 keys
-            if (!(p.dbg & 32)) tc::mma_bf16_ss_w(tmem + C::T_DQ, tc::smem_desc(ds_base + kk * 2048, 16384, 1024, tc::kSwizzle128B),
-                              tc::smem_desc(k_base + kk * 2048, 128 * 128, 1024, tc::kSwizzle128B), idesc_q, kk > 0);
-          tc::mma_commit_w(&dq_full[q & 1]);
-        }
-      }
-      tc::mma_commit_w(done);
-    }
-  } else if (warp >= 4) {
-    const int quarter = warp & 3, g = (warp - 4) >> 2;
-    const int r = quarter * 32 + lane;  // key row
-    const int64_t kpos = j0 + r;
-    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    tc::mbar_wait(kv_full, 0);
-    row_part_smem_to_tmem<HD>(tmem + lane_base + (g < 2 ? C::T_V : C::T_K) + (g & 1) * (HD / 4), g < 2 ? sV : sK, 128,
-                              r, g & 1);  // groups 0/1: V halves, 2/3: K halves (K also stays in SMEM for dQ)
-    tc::tmem_st_wait();
-    tc::tc_fence_before();
-    warp_arrive(v_tmem);
-    tc::mbar_wait(v_tmem, 0);  // sV becomes dS^T buffer 0: every copy must have read it
-    // dQ pair q drain: TMEM lane = query of the pair (32*quarter + lane), 16-column chunks
-    // c = g, g + 4 of the 80; rows past n are skipped.
-    // dQ pair q: TMEM (lane = query of the pair, 16-column chunks c = g, g + 4) ->
-    // registers (TMEM released at once) -> fp32 staging tile -> one TMA reduce-add
-    // into the [n, h] workspace (rows past n clipped by the map). Per-element
-    // red.global.add measured ~3.5 ms slower per long-prefix call: L2 atomics.
-    // Staging layout = the reduce boxes: columns 0-31 and 32-63 as [128 x 128 B] 128-byte
-    // swizzled tiles, 64-79 as a [128 x 64 B] 64-byte swizzled tile (conflict-free stores).
-    auto drain = [&](int q) {
-      tc::mbar_wait(&dq_full[q & 1], (q >> 1) & 1);
-      tc::tc_fence_after();
-      uint32_t v[2][16];
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-        if (g + 4 * k < HD / 16) tmem_ld16(tmem + lane_base + C::T_DQ + (g + 4 * k) * 16, v[k]);
-      tc::tmem_ld_wait();
-      tc::tc_fence_before();
-      warp_arrive(dq_free);
-      if (q >= 1) {  // pair q-1's reduce (issued by warp 4, lane 0) must have read the tile
-        if (warp == 4 && lane == 0) {
-          tc::bulk_wait_read0();
-          tc::mbar_arrive(stage_free);
-        }
-        tc::mbar_wait(stage_free, (q - 1) & 1);
-      }
-      const int rr = quarter * 32 + lane;  // query row of the pair
-      uint8_t* stage = reinterpret_cast<uint8_t*>(sDQ);
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int c = g + 4 * k;
-        if (c < HD / 16) {
-#pragma unroll
-          for (int e = 0; e < 16; e += 4) {
-            uint8_t* dst;
-            if (c < 4) {
-              const int u = (c & 1) * 4 + e / 4;  // 16-byte unit within the 128-byte row
-              dst = stage + (c >> 1) * 16384 + rr * 128 + ((u ^ (rr & 7)) << 4);
-            } else {
-              const int u = e / 4;
-              dst = stage + 32768 + rr * 64 + ((u ^ ((rr >> 1) & 3)) << 4);
-            }
-            *reinterpret_cast<float4*>(dst) =
-                make_float4(__uint_as_float(v[k][e]), __uint_as_float(v[k][e + 1]), __uint_as_float(v[k][e + 2]),
-                            __uint_as_float(v[k][e + 3]));
-          }
-        }
-      }
-      tc::fence_proxy_async_smem();
-      warp_arrive(stage_full);
-      if (warp == 4) {  // all 16 warps staged: one thread issues the pair's reduce-adds
-        tc::mbar_wait(stage_full, q & 1);
-        if (lane == 0 && !(p.dbg & 16)) {
-          const int row0 = static_cast<int>(ib0 + static_cast<int64_t>(q) * 128);
-          tc::tma_reduce_add_2d(&p.tdq, sDQ, head * HD, row0);
-          tc::tma_reduce_add_2d(&p.tdq, sDQ + 128 * 32, head * HD + 32, row0);
-          tc::tma_reduce_add_2d(&p.tdq16, sDQ + 128 * 64, head * HD + 64, row0);
-          tc::bulk_commit();
-        }
-      }
-    };
-    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-    for (int it = 0; it < niter; ++it) {
-      const int b = it % NS, st = it % QST;
-      const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
-      const float* nl = sLD + st * 128 + g * 16;
-      const float* nd = nl + 64;
-      const int64_t cbase = i0 + g * 16;
-      const int64_t cmin = kpos - p.q_off - cbase;
-      const int c_lo = cmin < 0 ? 0 : (cmin > 16 ? 16 : static_cast<int>(cmin));
-      const int64_t chi = p.n - cbase;
-      const int c_hi = chi < 0 ? 0 : (chi > 16 ? 16 : static_cast<int>(chi));
-      const bool full_blk = __all_sync(0xffffffffu, c_lo == 0 && c_hi == 16);
-      tc::mbar_wait(&q_full[st], (it / QST) & 1);
-      uint32_t sv[16], dpv[16];
-      tc::mbar_wait(&s_full[b], (it / NS) & 1);
-      tc::tc_fence_after();
-      tmem_ld16(tmem + lane_base + b * 64 + g * 16, sv);
-      tc::mbar_wait(dp_full, it & 1);
-      tc::tc_fence_after();
-      tmem_ld16(tmem + lane_base + C::T_DP + g * 16, dpv);
-      tc::tmem_ld_wait();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(dp_free);
-      uint32_t wp[8], wd[8];
-      auto body = [&](auto masked) {
-#pragma unroll
-        for (int e = 0; e < 16; e += 4) {
-          const float4 l4 = lds_f4(nl + e), d4 = lds_f4(nd + e);
-          const bool poly = bwd_poly_group(2 * (e / 4));
-          float2 p0 = ex2x2_sel(poly, ffma2(u2f2(sv[e], sv[e + 1]), sc2, make_float2(l4.x, l4.y)));
-          float2 p1 = ex2x2_sel(poly, ffma2(u2f2(sv[e + 2], sv[e + 3]), sc2, make_float2(l4.z, l4.w)));
-          if constexpr (decltype(masked)::value) {
-            if (e < c_lo || e >= c_hi) p0.x = 0.f;
-            if (e + 1 < c_lo || e + 1 >= c_hi) p0.y = 0.f;
-            if (e + 2 < c_lo || e + 2 >= c_hi) p1.x = 0.f;
-            if (e + 3 < c_lo || e + 3 >= c_hi) p1.y = 0.f;
-          }
-          const float2 g0 = fmul2(p0, fadd2(u2f2(dpv[e], dpv[e + 1]), make_float2(d4.x, d4.y)));
-          const float2 g1 = fmul2(p1, fadd2(u2f2(dpv[e + 2], dpv[e + 3]), make_float2(d4.z, d4.w)));
-          wp[e / 2] = pack2(p0);
-          wp[e / 2 + 1] = pack2(p1);
-          wd[e / 2] = pack2(g0);
-          wd[e / 2 + 1] = pack2(g1);
-        }
-      };
-      if (full_blk)
-        body(std::false_type{});
-      else
-        body(std::true_type{});
-      tc::tmem_st8(tmem + lane_base + b * 64 + g * 16, wp);
-      tc::tmem_st8(tmem + lane_base + b * 64 + g * 16 + 8, wd);
-      if (!(p.dbg & 64)) {  // dS^T row r, queries [16g, 16g+16) of this block -> MN-major A tile of dQ (SW128)
-        uint8_t* ds = (((it >> 1) & 1) ? sDS1 : sV) + (it & 1) * 16384 + r * 128;
-        const int u0 = (2 * g) ^ (r & 7), u1 = (2 * g + 1) ^ (r & 7);
-        *reinterpret_cast<uint4*>(ds + u0 * 16) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-        *reinterpret_cast<uint4*>(ds + u1 * 16) = make_uint4(wd[4], wd[5], wd[6], wd[7]);
-        if (!(p.dbg & 128)) tc::fence_proxy_async_smem();
-      }
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      warp_arrive(&sm_done[b]);
-      if (it >= 3 && (it & 1)) drain((it - 3) >> 1);  // pair q drained after block 2q + 3
-    }
-    tc::mbar_wait(done, 0);
-    tc::tc_fence_after();
-    drain(npair - 1);  // the last pair (earlier ones were drained inside the loop)
-    if (warp == 4 && lane == 0) tc::bulk_wait_read0();  // SMEM must outlive the last reduce
-    float* out = reinterpret_cast<float*>(sm);
-    constexpr int NCH = HD / 16;
-    for (int t = g; t < 2 * NCH; t += 4) {
-      const bool is_k = t >= NCH;
-      const int c = is_k ? t - NCH : t;
-      uint32_t v[16];
-      tmem_ld16(tmem + lane_base + (is_k ? C::T_DK : C::T_DV) + c * 16, v);
-      tc::tmem_ld_wait();
-      const float sc = is_k ? p.scale : 1.f;
-      float* dst = out + (is_k ? 0 : 128 * HD) + r * HD + c * 16;
-#pragma unroll
-      for (int e = 0; e < 16; e += 4)
-        *reinterpret_cast<float4*>(dst + e) =
-            make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
-                        __uint_as_float(v[e + 3]) * sc);
-    }
-    tc::fence_proxy_async_smem();
-    tc::named_bar_sync(1, 512);
-    if (warp == 4 && lane == 0) {
-      tc::tma_reduce_add_2d(&p.tdkv, out, head * HD, static_cast<int>(j0));
-      tc::tma_reduce_add_2d(&p.tdkv, out + 128 * HD, p.h + head * HD, static_cast<int>(j0));
-      tc::bulk_commit();
-      tc::bulk_wait_read0();
-    }
-  }
-  tc::tc_fence_before();
-  tc::cluster_sync();
-  tc::tc_fence_after();
-  if (warp == 1) tc::tmem_dealloc(tmem, 512);
-}
-
-// dq = bf16(dqf * scale): the fused kernel's fp32 dQ sums -> the bf16 output.
-__global__ void dq_cast_k(const float4* __restrict__ dqf, uint2* __restrict__ dq, int64_t n4, float scale) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 v = dqf[i];
-    dq[i] = make_uint2(pack_bf16(v.x * scale, v.y * scale), pack_bf16(v.z * scale, v.w * scale));
-  }
-}
-
 // ld: per head, blocks of 64 queries laid out as [64 x -LSE*log2e][64 x -delta],
 // delta = sum_d dO*O; zeros up to n_pad. One thread per (query, head), heads
 // fastest: a warp reads whole 16-byte vectors of one query row (coalesced through
@@ -1668,10 +1252,7 @@ void make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 // Chunk maps of a [outer, inner] bf16 tensor for [rows x hd] tiles.
 void make_maps(Maps* t, const void* ptr, uint64_t inner, uint64_t outer, int hd, uint32_t rows) {
   make_map(&t->m0, ptr, inner, outer, inner, 64, rows, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (hd == 80 && Lay<80>::NARROW)
-    make_map(&t->m1, ptr, inner, outer, inner, 16, rows, CU_TENSOR_MAP_SWIZZLE_32B);
-  else
-    t->m1 = t->m0;  // second chunk = another 64-wide SW128 box (hd 80: padded); hd 64: unused
+  t->m1 = t->m0;  // second chunk = another 64-wide SW128 box (hd 80: padded); hd 64: unused
 }
 
 }  // namespace
@@ -1795,11 +1376,13 @@ void attn_bwd_tc(bool dkv_overwrite, const void* q, const void* kv, const void* 
   a.h = h;
   a.scale = 1.f / sqrtf(static_cast<float>(hd));
   a.scale_log2 = 1.4426950408889634f * a.scale;
-  static const int dbg = [] {
+  a.dbg = 0;
+  a.trace = nullptr;
+#if SPK_ATTN_PROFILING
+  a.dbg = [] {
     const char* e = std::getenv("SP_ATTN_DBG");
     return e ? std::atoi(e) : 0;
   }();
-  a.dbg = dbg;
   static unsigned long long* trace_buf = [] {
     unsigned long long* t = nullptr;
     if (std::getenv("SP_ATTN_TRACE")) SPK_CUDA(cudaMalloc(&t, 16 * 64 * sizeof(unsigned long long)));
@@ -1807,59 +1390,10 @@ void attn_bwd_tc(bool dkv_overwrite, const void* q, const void* kv, const void* 
   }();
   a.trace = trace_buf;
   if (trace_buf) SPK_CUDA(cudaMemsetAsync(trace_buf, 0, 16 * 64 * sizeof(unsigned long long), s));
+#endif
   AttnBwdParams b = a;  // dQ kernel: K/V in 64-row tiles (Q / dO go to TMEM from the raw rows)
   b.trace = nullptr;
   make_maps(&b.tkv, kv, 2 * h, kv_len, hd, 64);
-  // Experimental (off by default; SP_ATTN_FUSED_BWD=1): the fused dK/dV/dQ kernel is
-  // parity-green but 6-10 % slower at the cfg-2 shapes -- shared-memory bandwidth
-  // bound (SS S^T and dQ MMAs plus dQ staging ~146 KB per iteration vs ~72 KB).
-  static const bool fused_env = [] {
-    const char* e = std::getenv("SP_ATTN_FUSED_BWD");
-    return e ? std::atoi(e) != 0 : false;
-  }();
-  if (hd == 80 && fused_env && ws_dq) {
-    constexpr int HD = 80;
-    if (dkv_overwrite) SPK_CUDA(cudaMemsetAsync(dkv, 0, sizeof(float) * static_cast<size_t>(kv_len) * 2 * h, s));
-    constexpr size_t smem = fused_smem_n<HD>(fused_stages<HD>());
-    static_assert(smem <= 232448, "fused attention bwd smem");
-    a.dqf = ws_dq;
-    SPK_CUDA(cudaMemsetAsync(ws_dq, 0, sizeof(float) * static_cast<size_t>(n) * h, s));
-    {
-      cuuint64_t dims[2] = {static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
-      cuuint64_t strides[1] = {static_cast<cuuint64_t>(h) * 4};
-      cuuint32_t box[2] = {32, 128}, box16[2] = {16, 128};
-      cuuint32_t estr[2] = {1, 1};
-      CUresult r = tma_encode_fn()(&a.tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ws_dq, dims, strides, box, estr,
-                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r == CUDA_SUCCESS)
-        r = tma_encode_fn()(&a.tdq16, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ws_dq, dims, strides, box16, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (dq) failed: " + std::to_string((int)r));
-    }
-    SPK_CUDA(cudaFuncSetAttribute(attn_bwd_fused_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const unsigned nkb2 = static_cast<unsigned>(((kv_len + 127) / 128 + 1) & ~int64_t(1));
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(nkb2, static_cast<unsigned>(H));
-    lc.blockDim = dim3(640);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    SPK_CUDA(cudaLaunchKernelEx(&lc, attn_bwd_fused_k<HD>, a));
-    const int64_t n4 = static_cast<int64_t>(n) * h / 4;
-    const int64_t blocks = (n4 + 255) / 256 < 8 * 148 ? (n4 + 255) / 256 : 8 * 148;
-    dq_cast_k<<<static_cast<unsigned>(blocks > 0 ? blocks : 1), 256, 0, s>>>(
-        reinterpret_cast<const float4*>(ws_dq), reinterpret_cast<uint2*>(dq), n4, a.scale);
-    SPK_LAUNCH_CHECK();
-    return;
-  }
   auto run = [&](auto hd_tag) {
     constexpr int HD = decltype(hd_tag)::value;
     constexpr size_t smem_dkv = dkv_smem<HD>(), smem_dq = dq_smem<HD>();
@@ -1884,7 +1418,7 @@ void attn_bwd_tc(bool dkv_overwrite, const void* q, const void* kv, const void* 
         const char* e = std::getenv("SP_ATTN_BWD_CONCURRENT");  // tuning: 0 = dQ after dK/dV in stream order
         return e ? std::atoi(e) != 0 : true;
       }();
-      if (concurrent && !trace_buf) {  // dQ first (long CTAs), on the side stream
+      if (concurrent && !a.trace) {  // dQ first (long CTAs), on the side stream
         SideStream& ss = side_stream();
         SPK_CUDA(cudaEventRecord(ss.fork, s));
         SPK_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
@@ -1897,9 +1431,10 @@ void attn_bwd_tc(bool dkv_overwrite, const void* q, const void* kv, const void* 
         return;
       }
       SPK_CUDA(cudaLaunchKernelEx(&lc, attn_bwd_dkv_k<HD>, a));
-      if (trace_buf) {
+#if SPK_ATTN_PROFILING
+      if (a.trace) {
         unsigned long long h_t[16 * 64];
-        SPK_CUDA(cudaMemcpyAsync(h_t, trace_buf, sizeof(h_t), cudaMemcpyDeviceToHost, s));
+        SPK_CUDA(cudaMemcpyAsync(h_t, a.trace, sizeof(h_t), cudaMemcpyDeviceToHost, s));
         SPK_CUDA(cudaStreamSynchronize(s));
         unsigned long long t0 = ~0ULL;
         for (unsigned long long v : h_t)
@@ -1913,6 +1448,7 @@ void attn_bwd_tc(bool dkv_overwrite, const void* q, const void* kv, const void* 
           std::fprintf(stderr, "\n");
         }
       }
+#endif
     }
     dim3 g2(static_cast<unsigned>((n + 127) / 128), static_cast<unsigned>(H));
     attn_bwd_dq_k<HD><<<g2, 640, smem_dq, s>>>(b);

@@ -254,7 +254,8 @@ __global__ void fill_const_k(float* p, int64_t n, float v) {
 
 template <typename T>
 __global__ void adamw_k(float* p, const float* __restrict__ g, float* m, float* v, T* pc, int64_t n, float lr, float b1,
-                        float b2, float eps, float wd, float bc1, float bc2) {
+                        float b2, float eps, float wd, const float* __restrict__ bc) {
+  const float bc1 = bc[0], bc2 = bc[1];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i];
     const float mi = b1 * m[i] + (1.f - b1) * gi;
@@ -272,7 +273,8 @@ __global__ void adamw_k(float* p, const float* __restrict__ g, float* m, float* 
 // per parameter, HBM bound).
 template <typename T>
 __global__ void adamw_vec_k(float4* p, const float4* __restrict__ g, float4* m, float4* v, T* pc, int64_t n4, float lr,
-                            float b1, float b2, float eps, float wd, float bc1, float bc2) {
+                            float b1, float b2, float eps, float wd, const float* __restrict__ bc) {
+  const float bc1 = bc[0], bc2 = bc[1];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 gi = g[i];
     float4 mi = m[i], vi = v[i], pi = p[i];
@@ -920,17 +922,16 @@ void fill_const(float* p, int64_t n, float v, cudaStream_t s) {
 }
 
 void adamw(float* p, const float* g, float* m, float* v, void* pc, DType t, int64_t n, float lr, float b1, float b2,
-           float eps, float wd, int step, cudaStream_t s) {
-  const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
+           float eps, float wd, const float* bc, cudaStream_t s) {
   const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
   if (n % 4 == 0 && al16(p) && al16(g) && al16(m) && al16(v)) {
     SPK_DISPATCH(t, adamw_vec_k<T><<<stream_grid(n / 4, 256), 256, 0, s>>>(
                         reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g), reinterpret_cast<float4*>(m),
-                        reinterpret_cast<float4*>(v), (T*)pc, n / 4, lr, b1, b2, eps, wd, bc1, bc2));
+                        reinterpret_cast<float4*>(v), (T*)pc, n / 4, lr, b1, b2, eps, wd, bc));
     SPK_LAUNCH_CHECK();
     return;
   }
-  SPK_DISPATCH(t, adamw_k<T><<<stream_grid(n, 256), 256, 0, s>>>(p, g, m, v, (T*)pc, n, lr, b1, b2, eps, wd, bc1, bc2));
+  SPK_DISPATCH(t, adamw_k<T><<<stream_grid(n, 256), 256, 0, s>>>(p, g, m, v, (T*)pc, n, lr, b1, b2, eps, wd, bc));
   SPK_LAUNCH_CHECK();
 }
 

@@ -540,9 +540,13 @@ void gemm_tcgen05(const GemmArgs& a, cudaStream_t s) {
 
 void gemm(const GemmArgs& a, cudaStream_t s, int impl) {
   if (a.M == 0 || a.N == 0) return;
+  // fp32 validation mode (or an explicit SIMT request) -> SIMT; bf16 -> tcgen05 only. A bf16
+  // shape the tensor-core path cannot take is an error, never a silent SIMT fallback.
   if (impl == kGemmSimt || a.ab == DType::kF32) return gemm_simt(a, s);
-  if (impl == kGemmTcgen05 || gemm_tc_supported(a)) return gemm_tcgen05(a, s);
-  gemm_simt(a, s);
+  if (!gemm_tc_supported(a))
+    throw std::invalid_argument("gemm: bf16 operands need 16-byte aligned pointers and row strides (multiples of 8 "
+                                "elements) for the tcgen05/TMA path; no SIMT fallback in bf16 mode");
+  gemm_tcgen05(a, s);
 }
 
 }  // namespace spk

@@ -92,7 +92,8 @@ void ce_fwd_bwd(DType t, void* logits, int64_t ld, const int32_t* labels, int64_
 void cast_from_f32(DType t, const float* src, void* dst, int64_t n, cudaStream_t s);
 void fill_normal(float* p, int64_t n, uint64_t seed, float stddev, cudaStream_t s);
 void fill_const(float* p, int64_t n, float v, cudaStream_t s);
+// bc: device {1 - b1^t, 1 - b2^t} (so a captured step graph replays with the current t).
 void adamw(float* p, const float* g, float* m, float* v, void* pc, DType t, int64_t n, float lr, float b1, float b2,
-           float eps, float wd, int step, cudaStream_t s);
+           float eps, float wd, const float* bc, cudaStream_t s);
 
 }  // namespace spk

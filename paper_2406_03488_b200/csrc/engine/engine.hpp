@@ -5,7 +5,6 @@
 #pragma once
 
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <map>
 #include <memory>
@@ -14,6 +13,7 @@
 
 #include "cuda/common.cuh"
 #include "cuda/ops.h"
+#include "engine/transport.hpp"
 #include "seqpipe/partition.hpp"
 #include "seqpipe/scenario.hpp"
 #include "seqpipe/schedule.hpp"
@@ -142,7 +142,9 @@ class Stage {
   void set_flags(int f) { mc_.flags = f; }
   void zero_grads();
   void sync_compute();  // recast the compute-dtype weight copy after a master write
-  void optimizer_step(int step);
+  // AdamW over this stage's parameters; bias corrections {1-b1^t, 1-b2^t} read from device memory
+  // (written per step outside any captured graph).
+  void optimizer_step(const float* bc_dev);
   void init_weights();
   const std::vector<Param>& params() const { return params_; }
   float* master() const { return master_; }
@@ -155,6 +157,8 @@ class Stage {
   // micro-batch's KV-prefix slab: the units of the measured memory series.
   int64_t record_bytes(int s) const;
   int64_t kv_slab_bytes() const;
+  // Planned bytes of one zero-bubble W record (operands I leaves for W) of segment s.
+  int64_t w_record_bytes(int s) const;
   double dkv_bytes() const { return static_cast<double>(L_s_) * T_ * 2 * mc_.h * 4; }
   int stage() const { return stage_; }
   bool first() const { return stage_ == 1; }
@@ -219,8 +223,14 @@ class Engine {
   Engine(const seqpipe::ScenarioConfig& cfg, seqpipe::ScheduleKind kind, const std::vector<int64_t>& lengths,
          const ModelCfg& m, int rank, int world, int cuda_device);
   ~Engine();
+  // Multi-rank data plane: NCCL communicators from `ids` (one per channel), or an in-process hub.
   void comm_init(const std::vector<std::string>& ids);
+  void attach_local(std::shared_ptr<LocalHub> hub);
+  int comm_channels() const;
   void step(const int32_t* tokens, bool on_device, sp_step_report* rep);
+  // Capture the step (ops + optimizer) once into a CUDA graph and replay it (single-rank engines).
+  void enable_graph(bool on);
+  bool graph_active() const { return graph_exec_ != nullptr; }
   const std::vector<seqpipe::Task>& op_log() const { return op_log_; }
   std::vector<std::vector<seqpipe::Task>> op_log_by_device() const;
   const std::vector<double>& t_start() const { return t_start_; }
@@ -233,15 +243,34 @@ class Engine {
   Stage* stage_for_param(const std::string& name, Param* out);
   std::vector<std::pair<Stage*, Param>> all_params();
   int device() const { return dev_; }
+  bool table_from_device() const { return table_from_device_; }
   void set_flags(int f) {
     mc_.flags = f;
     for (auto& kv : stages_) kv.second->set_flags(f);
   }
 
  private:
+  void enqueue_ops();  // every op of this process's order (+ transfers), on the engine streams
   void exec_op(const seqpipe::Task& t, int order_index, int device_pos);
+  // Receive side of one channel: R staging slots so receives are posted ahead of the op that
+  // consumes them (the op copies the message out of its slot on the compute stream).
+  struct RecvChannel {
+    int peer = -1;
+    cudaStream_t s = nullptr;
+    std::vector<void*> slot;
+    std::vector<cudaEvent_t> done, freed;  // recv completed / slot consumed
+    std::vector<const sp_comm_op*> msgs;   // this step's messages in order
+    size_t posted = 0, consumed = 0;
+  };
+  static constexpr int kRecvSlots = 2;
+  void post_recvs(RecvChannel& rc, int ch, bool block_for_next);
+  std::map<int, RecvChannel> recv_ch_;
+  std::map<int, cudaStream_t> send_s_;  // per send channel
   std::vector<std::vector<sp_comm_op>> plan_pre_, plan_post_;  // per device-order position
+  std::vector<sp_comm_op> plan_;
   Stage* stage_obj(int stage) { return stages_.at(stage).get(); }
+  void comm_ready_setup();
+  void drop_graph();
 
   seqpipe::ScenarioConfig cfg_;
   seqpipe::ScheduleKind kind_;
@@ -249,25 +278,35 @@ class Engine {
   ModelCfg mc_;
   int rank_, world_, dev_;
   seqpipe::Schedule sched_;
+  bool table_from_device_ = false;
   std::vector<std::pair<int, int>> replay_;  // (device, position) execution order for this process
   std::map<int, std::unique_ptr<Stage>> stages_;
-  cudaStream_t s_ = nullptr, s_send_ = nullptr, s_recv_ = nullptr;
+  cudaStream_t s_ = nullptr;
   int32_t* tokens_dev_ = nullptr;
   int32_t* tokens_owned_ = nullptr;
   double* loss_dev_ = nullptr;
+  float* adam_bc_dev_ = nullptr;   // {1 - b1^t, 1 - b2^t} of the current step (device)
+  float* adam_bc_host_ = nullptr;  // pinned staging for it
   int step_no_ = 0;
   std::vector<seqpipe::Task> op_log_;
   std::vector<cudaEvent_t> ev_start_, ev_end_;
   cudaEvent_t ev_step0_ = nullptr, ev_step1_ = nullptr;
   std::vector<double> t_start_, t_end_;
-  // NCCL: [0] activations on even edges, [1] odd edges, [2] grads even, [3] grads odd
-  ncclComm_t comms_[4] = {nullptr, nullptr, nullptr, nullptr};
-  bool comm_ready_ = false;
+  std::unique_ptr<Transport> transport_;
   std::vector<void*> send_ring_;
   std::vector<cudaEvent_t> send_ring_ev_;
   int send_ring_next_ = 0;
+  std::vector<cudaEvent_t> act_sent_;  // per (m,s) of a sending stage: activation send retired
   cudaEvent_t ev_tmp_ = nullptr;
+  double watchdog_s_ = 600.0;
   KernelProbe probe_;
+  // CUDA graph of the step body (world == 1)
+  bool graph_wanted_ = false;
+  int graph_flags_ = 0;
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  int64_t graph_launches_ = 0;  // kernels in the captured step body
+  double graph_flops_ = 0;
 };
 
 }  // namespace spe

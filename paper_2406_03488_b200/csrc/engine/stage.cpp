@@ -219,10 +219,10 @@ void Stage::sync_compute() {
 
 void Stage::zero_grads() { SPK_CUDA(cudaMemsetAsync(grad_, 0, sizeof(float) * nparams_, s_)); }
 
-void Stage::optimizer_step(int step) {
+void Stage::optimizer_step(const float* bc_dev) {
   if (mc_.lr <= 0.f) return;
   spk::adamw(master_, grad_, adam_m_, adam_v_, compute_ == master_ ? nullptr : compute_, mc_.dt, nparams_, mc_.lr,
-             mc_.b1, mc_.b2, mc_.adam_eps, mc_.wd, step, s_);
+             mc_.b1, mc_.b2, mc_.adam_eps, mc_.wd, bc_dev, s_);
   ++launches;
 }
 
@@ -294,6 +294,7 @@ DualArena plan_stage_memory(const ModelCfg& mc, const seqpipe::ScenarioConfig& c
 }
 
 int64_t Stage::record_bytes(int s) const { return seg_bytes(mc_, L_s_, len_[static_cast<size_t>(s - 1)], esz_); }
+int64_t Stage::w_record_bytes(int s) const { return w_bytes(mc_, L_s_, len_[static_cast<size_t>(s - 1)], esz_); }
 int64_t Stage::kv_slab_bytes() const { return static_cast<int64_t>(L_s_) * T_ * 2 * mc_.h * static_cast<int64_t>(esz_); }
 
 void Stage::plan_arena(const std::vector<seqpipe::Task>& order) {
@@ -371,8 +372,7 @@ void Stage::wgrad(const GemmArgs& a, double flop) {
     const char* e = std::getenv("SP_WGRAD_STREAM");  // tuning: 0 = weight gradients in stream order
     return e ? std::atoi(e) != 0 : true;
   }();
-  // Kernel probes time each GEMM on the compute stream; keep stream order then.
-  if (!side || (probe && probe->enabled) || (mc_.flags & SP_FLAG_NO_TCGEN05) || mc_.dt == DType::kF32) {
+  if (!side || (mc_.flags & SP_FLAG_NO_TCGEN05) || mc_.dt == DType::kF32) {
     gemm(a, flop);
     return;
   }
@@ -383,7 +383,9 @@ void Stage::wgrad(const GemmArgs& a, double flop) {
   }
   SPK_CUDA(cudaEventRecord(ev_fork_, s_));
   SPK_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
+  if (probe && probe->enabled) probe->begin(KernelProbe::kGemm, s2_, flop);  // timed on its own stream
   spk::gemm(a, s2_, spk::kGemmAuto);
+  if (probe && probe->enabled) probe->end(s2_);
   SPK_CUDA(cudaEventRecord(ev_join_, s2_));
   pending_join_ = true;
   flops += flop;

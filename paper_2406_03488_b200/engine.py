@@ -88,9 +88,31 @@ class Engine:
         self.model.flags = flags
         _check(_capi.lib().sp_engine_set_flags(self._h, flags))
 
+    def comm_channels(self) -> int:
+        """Number of P2P channels (pipeline edges x 2 directions): NCCL ids comm_init needs."""
+        n = C.c_int32()
+        _check(_capi.lib().sp_engine_comm_channels(self._h, C.byref(n)))
+        return n.value
+
     def comm_init(self, ids: list):
+        """NCCL data plane: one unique id per channel (rank 0 creates them, every rank passes all)."""
         arr = (C.c_char_p * len(ids))(*ids)
         _check(_capi.lib().sp_engine_comm_init(self._h, arr, len(ids)))
+
+    def attach_local(self, hub: "LocalHub"):
+        """In-process data plane: several engines of one process (one host thread each)."""
+        self._hub = hub  # keep the hub alive as long as the engine
+        _check(_capi.lib().sp_engine_attach_local(self._h, hub._h))
+
+    def enable_graph(self, on: bool = True):
+        """Capture the step body into a CUDA graph on the next step and replay it (world size 1)."""
+        _check(_capi.lib().sp_engine_enable_graph(self._h, 1 if on else 0))
+
+    def memory(self):
+        """(bytes allocated on the engine's device, bytes free) after a synchronize."""
+        a, f = C.c_double(), C.c_double()
+        _check(_capi.lib().sp_engine_memory(self._h, C.byref(a), C.byref(f)))
+        return a.value, f.value
 
     def step(self, tokens, on_device: bool = False) -> _capi.StepReport:
         """One training step (all micro-batches, optimizer included). tokens: int32 [M, T+1]
@@ -173,6 +195,22 @@ class Engine:
         v = np.ascontiguousarray(value, dtype=np.float32)
         _check(_capi.lib().sp_engine_write_param(self._h, name.encode(), v.ctypes.data_as(C.POINTER(C.c_float)),
                                                  v.size))
+
+
+class LocalHub:
+    """In-process P2P hub shared by the `world_size` engines of one process (sp_local_hub_*)."""
+
+    def __init__(self, world_size: int, watchdog_seconds: float = 120.0):
+        self._h = C.c_void_p()
+        _check(_capi.lib().sp_local_hub_create(world_size, watchdog_seconds, C.byref(self._h)))
+
+    def __del__(self):
+        try:
+            if self._h:
+                _capi.lib().sp_local_hub_destroy(self._h)
+                self._h = C.c_void_p()
+        except Exception:
+            pass
 
 
 def plan_memory(cfg: pl.ScenarioConfig, kind, partition: pl.SequencePartition, model: ModelConfig, stage: int = 1):

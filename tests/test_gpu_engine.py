@@ -210,6 +210,19 @@ def test_zero_bubble_input_weight_split(gpu, kind, k, dtype, tol):
 
 
 
+def test_zero_bubble_deep_pipeline_no_record_reuse_race(gpu):
+    """SeqZB1P at P=4 M=8 k=4 (even partition): W(m,s,v) runs after W(m,s,v-1) on this
+    schedule, so stage v's layer-0 input must not alias stage v-1's (freed, reused) output
+    record. fp32 step vs the oracle catches any stale read."""
+    model = tiny_model(layers=4, hidden=128, heads=2, ffn=256, vocab=256, max_seq=512)
+    cfg = scenario(model, P=4, M=8, k=4, T=512)
+    eng, part, tok, rep = run(model, cfg, kind="seqzb1p", mode="even")
+    log = eng.op_log()
+    assert log.device_orders == ref.generate(cfg, "seqzb1p", part).device_orders
+    compare(eng, model, part, tok, rep, TOL_F32)
+    eng.close()
+
+
 def test_adamw_update_matches_formula(gpu):
     """One AdamW step (elementwise.cu adamw kernels) == the closed form at step 1:
     m = (1-b1) g, v = (1-b2) g^2, p -= lr ((m/bc1) / (sqrt(v/bc2) + eps) + wd p)."""
@@ -257,4 +270,37 @@ def test_bf16_gpt_2p7b_width_hd80(gpu):
     cfg = scenario(model, P=1, M=2, k=2, T=512)
     eng, part, tok, rep = run(model, cfg)
     compare(eng, model, part, tok, rep, TOL_BF16)
+    eng.close()
+
+
+def test_bf16_engine_step_at_benchmarked_cfg2_shape(gpu):
+    """One GPT-2.7B-width layer (h 2560, 32 x 80 heads, FFN 4h, vocab 50257) run through the
+    engine exactly at the benchmarked sequence shape: T = 32768 split by the cfg-2 cwp partition
+    [10170, 8496, 7428, 6674] (the gpt-2.7b preset with bench.py's overrides), bf16 production
+    kernels, M = 1. Loss and every parameter gradient vs the fp64 oracle (run on the GPU through
+    its torch backend, attention chunked over heads): relative L2 <= 2e-2."""
+    import torch
+    from oracle.transformer import TorchOps
+    bench_cfg = pl.preset_scenario("gpt-2.7b")
+    for k_, v_ in (("pipeline_size", "1"), ("seq_len", "32768"), ("segments", "4"), ("micro_batches", "8")):
+        pl.apply_scenario_override(bench_cfg, k_, v_)
+    lengths = pl.cwp_partition(bench_cfg).lengths
+    assert lengths == [10170, 8496, 7428, 6674]
+    model = E.ModelConfig(family=GPT, dtype=E.BF16, vocab=50257, hidden=2560, layers=1, heads=32, head_dim=80,
+                          ffn=4 * 2560, max_seq=32768, seed=42)
+    cfg = pl.ScenarioConfig(pipeline_size=1, micro_batches=1, segments=4, seq_len=32768, layers=1, hidden_dim=2560,
+                            param_count=model.param_count())
+    part = pl.make_partition(lengths, cfg)
+    eng = E.Engine(cfg, "seq1f1b", part, model)
+    tok = tokens_for(1, 32768, model.vocab, seed=1234)
+    rep = eng.step(tok)
+    params = {n: eng.read_param(n) for n in eng.params()}
+    oracle = Model(GPT, model.vocab, model.hidden, 1, 32, 80, model.ffn, ops=TorchOps("cuda"), head_chunk=2)
+    loss, grads = oracle.step(params, tok, lengths)
+    del oracle
+    torch.cuda.empty_cache()
+    assert abs(rep.loss - loss) / abs(loss) < TOL_BF16, (rep.loss, loss)
+    worst = {n: rel_l2(eng.read_grad(n), grads[n]) for n in params}
+    bad = {k: v for k, v in worst.items() if v > TOL_BF16}
+    assert not bad, (bad, worst)
     eng.close()

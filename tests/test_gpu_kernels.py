@@ -190,42 +190,65 @@ def test_activation_fwd_bwd(gpu, family, n, F):
     assert _rel(du.float(), uf.grad) < 1e-2
 
 
-FUSED_CHECK = r"""
-import ctypes as C, sys, torch
-sys.path.insert(0, '.')
-from paper_2406_03488_b200 import _capi
-n, q_off, H, hd = (int(x) for x in sys.argv[1:5])
-h, L = H * hd, q_off + n
-g = torch.Generator(device='cuda').manual_seed(n + q_off)
-q = (torch.randn(n, h, device='cuda', generator=g) * 0.5).to(torch.bfloat16)
-kv = (torch.randn(L, 2 * h, device='cuda', generator=g) * 0.5).to(torch.bfloat16)
-do = torch.randn(n, h, device='cuda', generator=g).to(torch.bfloat16)
-o = torch.empty_like(q); lse = torch.empty(H, n, device='cuda')
-dq = torch.empty_like(q); dkv = torch.zeros(L, 2 * h, device='cuda')
-P = lambda t: C.c_void_p(t.data_ptr())
-lib = _capi.lib()
-_capi.check(lib.sp_attention_fwd(1, 0, P(q), P(kv), P(o), P(lse), n, q_off, L, H, hd, None))
-_capi.check(lib.sp_attention_bwd(1, 0, P(q), P(kv), P(o), P(do), P(lse), P(dq), P(dkv), n, q_off, L, H, hd, None))
-torch.cuda.synchronize()
-torch.save({'dq': dq.float().cpu(), 'dkv': dkv.cpu()}, sys.argv[5])
-"""
+def _attn_ref_chunked(q, kv, dout, n, q_off, H, hd, chunk=2):
+    """fp64 reference of the prefix attention and its backward, head chunk by head chunk
+    (the full [H, n, kv] score tensor at the cfg-2 shapes would not fit)."""
+    h = H * hd
+    L = q_off + n
+    o = torch.empty(n, h, dtype=torch.float64, device="cuda")
+    lse = torch.empty(H, n, dtype=torch.float64, device="cuda")
+    dq = torch.empty_like(o)
+    dk = torch.empty(L, h, dtype=torch.float64, device="cuda")
+    dv = torch.empty_like(dk)
+    mask = torch.arange(L, device="cuda")[None, :] > (q_off + torch.arange(n, device="cuda"))[:, None]
+    for c0 in range(0, H, chunk):
+        sl = slice(c0 * hd, (c0 + chunk) * hd)
+        qh = q[:, sl].double().view(n, chunk, hd).transpose(0, 1)
+        kh = kv[:, :h][:, sl].double().view(L, chunk, hd).transpose(0, 1)
+        vh = kv[:, h:][:, sl].double().view(L, chunk, hd).transpose(0, 1)
+        doh = dout[:, sl].double().view(n, chunk, hd).transpose(0, 1)
+        S = (qh @ kh.transpose(1, 2) / hd ** 0.5).masked_fill(mask[None], float("-inf"))
+        lse[c0:c0 + chunk] = torch.logsumexp(S, dim=2)
+        P = torch.softmax(S, dim=2)
+        del S
+        oh = P @ vh
+        o[:, sl] = oh.transpose(0, 1).reshape(n, -1)
+        dP = doh @ vh.transpose(1, 2)
+        dS = P * (dP - (doh * oh).sum(-1, keepdim=True)) / hd ** 0.5
+        del dP
+        dv[:, sl] = (P.transpose(1, 2) @ doh).transpose(0, 1).reshape(L, -1)
+        del P
+        dq[:, sl] = (dS @ kh).transpose(0, 1).reshape(n, -1)
+        dk[:, sl] = (dS.transpose(1, 2) @ qh).transpose(0, 1).reshape(L, -1)
+        del dS
+    return o, lse, dq, dk, dv
 
 
-@pytest.mark.parametrize("n,q_off", [(700, 1111), (1000, 0), (96, 160)])
-def test_attention_bwd_fused_matches_split(gpu, tmp_path, n, q_off):
-    """Experimental fused dK/dV/dQ kernel (SP_ATTN_FUSED_BWD=1, head dim 80) == the default
-    dK/dV + dQ kernels on the same inputs (bf16 tolerance)."""
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
-    root = Path(__file__).resolve().parent.parent
-    outs = {}
-    for flag in ("0", "1"):
-        f = tmp_path / f"r{flag}.pt"
-        env = dict(os.environ, SP_ATTN_FUSED_BWD=flag)
-        subprocess.run([sys.executable, "-c", FUSED_CHECK, str(n), str(q_off), "2", "80", str(f)], cwd=root, env=env,
-                       check=True, timeout=300)
-        outs[flag] = torch.load(f)
-    for k in ("dq", "dkv"):
-        assert _rel(outs["1"][k], outs["0"][k]) < 1e-2, (k, _rel(outs["1"][k], outs["0"][k]))
+@pytest.mark.parametrize("n,q_off", [(10170, 0), (8496, 10170), (6674, 26094)])
+def test_attention_at_benchmarked_cfg2_shapes(gpu, n, q_off):
+    """The tcgen05 prefix attention at the exact shapes bench.py runs (GPT-2.7B: 32 heads x 80,
+    cfg-2 cwp sub-sequences [10170, 8496, 7428, 6674] of a 32K sequence): first sub-sequence at
+    prefix 0, second, and the last one over a 32768-row KV prefix. bf16 vs fp64, rel-L2 <= 2e-2
+    (north-star bf16 tolerance) for o, lse, dq, dK, dV."""
+    H, hd = 32, 80
+    h = H * hd
+    L = q_off + n
+    g = torch.Generator(device="cuda").manual_seed(n)
+    q = torch.randn(n, h, device="cuda", generator=g).to(torch.bfloat16)
+    kv = torch.randn(L, 2 * h, device="cuda", generator=g).to(torch.bfloat16)
+    dout = torch.randn(n, h, device="cuda", generator=g).to(torch.bfloat16)
+    o = torch.empty(n, h, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(H, n, device="cuda", dtype=torch.float32)
+    _capi.check(_capi.lib().sp_attention_fwd(BF16, 2, _p(q), _p(kv), _p(o), _p(lse), n, q_off, L, H, hd, None))
+    dq = torch.empty(n, h, device="cuda", dtype=torch.bfloat16)
+    dkv = torch.zeros(L, 2 * h, device="cuda", dtype=torch.float32)
+    _capi.check(_capi.lib().sp_attention_bwd(BF16, 2, _p(q), _p(kv), _p(o), _p(dout), _p(lse), _p(dq), _p(dkv), n,
+                                             q_off, L, H, hd, None))
+    torch.cuda.synchronize()
+    o_ref, lse_ref, dq_ref, dk_ref, dv_ref = _attn_ref_chunked(q, kv, dout, n, q_off, H, hd)
+    tol = 2e-2
+    assert _rel(o.float(), o_ref) < 1e-2
+    assert _rel(lse, lse_ref) < 1e-3
+    assert _rel(dq.float(), dq_ref) < tol
+    assert _rel(dkv[:, :h], dk_ref) < tol
+    assert _rel(dkv[:, h:], dv_ref) < tol

@@ -98,3 +98,17 @@ def test_split_equals_unsplit(family, lengths):
     lk, gk = m.step(p, tok, lengths)
     assert abs(l1 - lk) < 1e-12
     assert max(rel_l2(gk[k], g1[k]) for k in g1) < 1e-12
+
+
+@pytest.mark.parametrize("family", [GPT, LLAMA])
+def test_torch_backend_and_head_chunking_match_numpy(family):
+    """The oracle's torch-fp64 backend (used on the GPU box for the 32K-token parity
+    checks) and its head-chunked attention give the numpy oracle's numbers."""
+    from oracle.transformer import TorchOps
+    h, H, L, F, V, T = 64, 4, 2, 128, 97, 64
+    p = params(family, V, h, L, F, T, seed=5)
+    tok = tokens_for(2, T, V, seed=9)
+    l0, g0 = Model(family, V, h, L, H, h // H, F).step(p, tok, [30, 20, 14])
+    l1, g1 = Model(family, V, h, L, H, h // H, F, ops=TorchOps("cpu"), head_chunk=1).step(p, tok, [30, 20, 14])
+    assert abs(l0 - l1) < 1e-12
+    assert max(rel_l2(g1[k], g0[k]) for k in g0) < 1e-12

@@ -9,7 +9,11 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch  # noqa: E402
 from paper_2406_03488_b200 import _capi  # noqa: E402
 
-n, q_off, H, hd = (int(x) for x in (sys.argv[1:5] if len(sys.argv) > 4 else (6674, 26094, 32, 80)))
+args = sys.argv[1:]
+if args[:1] == ["--variant"]:  # a tuning build from tools/build_variant.py
+    _capi.LIB_PATH = _capi.LIB_PATH.parent / "variants" / f"libseqpipe_b200_{args[1]}.so"
+    args = args[2:]
+n, q_off, H, hd = (int(x) for x in (args[:4] if len(args) > 3 else (6674, 26094, 32, 80)))
 h, L = H * hd, q_off + n
 q = torch.randn(n, h, device="cuda").to(torch.bfloat16)
 kv = torch.randn(L, 2 * h, device="cuda").to(torch.bfloat16)

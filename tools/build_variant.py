@@ -1,8 +1,10 @@
 #!/usr/bin/env python
 """Build a tuning variant of the product library with extra nvcc defines for one
 CUDA source: tools/build_variant.py NAME SOURCE.cu -DFOO=1 ...  ->
-paper_2406_03488_b200/lib/variants/libseqpipe_b200_NAME.so (load it with
-SP_LIB_VARIANT=NAME). Used only for kernel tuning sweeps on the GPU box."""
+paper_2406_03488_b200/lib/variants/libseqpipe_b200_NAME.so. Used only for kernel
+tuning sweeps on the GPU box: a tool loads it by pointing _capi.LIB_PATH at it
+before the first _capi.lib() call (tools/attn_once.py --variant NAME); the
+product loader honours no environment switch."""
 import subprocess
 import sys
 from pathlib import Path
