@@ -163,7 +163,8 @@ Engine::~Engine() {
   for (auto e : ev_start_) cudaEventDestroy(e);
   for (auto e : ev_end_) cudaEventDestroy(e);
   for (auto e : send_ring_ev_) cudaEventDestroy(e);
-  for (auto e : act_sent_) cudaEventDestroy(e);
+  for (auto e : act_sent_)
+    if (e) cudaEventDestroy(e);  // only the F-send slots hold events
   for (auto p : send_ring_) cudaFree(p);
   for (auto& [c, rc] : recv_ch_) {
     for (void* p : rc.slot) cudaFree(p);
@@ -180,6 +181,7 @@ Engine::~Engine() {
   if (adam_bc_dev_) cudaFree(adam_bc_dev_);
   if (adam_bc_host_) cudaFreeHost(adam_bc_host_);
   if (s_) cudaStreamDestroy(s_);
+  (void)cudaGetLastError();  // teardown errors must not surface in the next API call of this thread
 }
 
 int Engine::comm_channels() const { return spe::comm_channels(cfg_); }
@@ -288,7 +290,9 @@ void Engine::exec_op(const seqpipe::Task& t, int i, int pos) {
   if (world_ > 1) {
     for (const sp_comm_op& c : plan_pre_[static_cast<size_t>(pos)]) {  // the op's input from the peer
       RecvChannel& rc = recv_ch_.at(c.channel);
-      if (rc.consumed >= rc.msgs.size() || rc.msgs[rc.consumed] != &c)
+      // plan_pre_ holds copies of the plan entries: compare the message, not its address.
+      if (rc.consumed >= rc.msgs.size() || rc.msgs[rc.consumed]->op_index != c.op_index ||
+          comm_entry_tag(*rc.msgs[rc.consumed]) != comm_entry_tag(c))
         throw std::logic_error("P2P: receive consumed out of plan order");
       post_recvs(rc, c.channel, /*block_for_next=*/true);
       const size_t slot = rc.consumed % kRecvSlots;

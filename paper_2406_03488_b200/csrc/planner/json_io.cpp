@@ -211,8 +211,14 @@ class Parser {
     ws();
     if (p_ >= t_.size()) fail("unexpected end");
     const char c = t_[p_];
-    if (c == '{') return object();
-    if (c == '[') return array();
+    if (c == '{' || c == '[') {
+      // Bounded nesting: schedule files come from users (`validate`), so deep
+      // input must be an error, not a stack overflow.
+      if (++depth_ > kMaxDepth) fail("nesting deeper than 256");
+      JValue v = c == '{' ? object() : array();
+      --depth_;
+      return v;
+    }
     if (c == '"') return JValue::Str(string());
     if (c == '-' || (c >= '0' && c <= '9')) return number();
     if (t_.compare(p_, 4, "true") == 0) {
@@ -280,16 +286,28 @@ class Parser {
         case 'r': out += '\r'; break;
         case 't': out += '\t'; break;
         case 'u': {
-          if (p_ + 4 > t_.size()) fail("bad \\u escape");
-          const unsigned cp = static_cast<unsigned>(std::stoul(t_.substr(p_, 4), nullptr, 16));
-          p_ += 4;
+          unsigned cp = hex4();
+          if (cp >= 0xD800 && cp < 0xDC00) {  // high surrogate: a low one must follow
+            if (p_ + 2 > t_.size() || t_[p_] != '\\' || t_[p_ + 1] != 'u') fail("unpaired surrogate");
+            p_ += 2;
+            const unsigned lo = hex4();
+            if (lo < 0xDC00 || lo >= 0xE000) fail("unpaired surrogate");
+            cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+          } else if (cp >= 0xDC00 && cp < 0xE000) {
+            fail("unpaired surrogate");
+          }
           if (cp < 0x80) {
             out += static_cast<char>(cp);
           } else if (cp < 0x800) {
             out += static_cast<char>(0xC0 | (cp >> 6));
             out += static_cast<char>(0x80 | (cp & 0x3F));
-          } else {
+          } else if (cp < 0x10000) {
             out += static_cast<char>(0xE0 | (cp >> 12));
+            out += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+            out += static_cast<char>(0x80 | (cp & 0x3F));
+          } else {
+            out += static_cast<char>(0xF0 | (cp >> 18));
+            out += static_cast<char>(0x80 | ((cp >> 12) & 0x3F));
             out += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
             out += static_cast<char>(0x80 | (cp & 0x3F));
           }
@@ -300,6 +318,20 @@ class Parser {
     }
     return out;
   }
+  // Exactly four hex digits (stoul would accept a partial "\u12G4").
+  unsigned hex4() {
+    if (p_ + 4 > t_.size()) fail("bad \\u escape");
+    unsigned v = 0;
+    for (int i = 0; i < 4; ++i) {
+      const char h = t_[p_++];
+      v <<= 4;
+      if (h >= '0' && h <= '9') v |= static_cast<unsigned>(h - '0');
+      else if (h >= 'a' && h <= 'f') v |= static_cast<unsigned>(h - 'a' + 10);
+      else if (h >= 'A' && h <= 'F') v |= static_cast<unsigned>(h - 'A' + 10);
+      else fail("bad \\u escape");
+    }
+    return v;
+  }
   JValue number() {
     const std::size_t b = p_;
     if (t_[p_] == '-') ++p_;
@@ -308,8 +340,10 @@ class Parser {
     if (p_ == b || (p_ == b + 1 && t_[b] == '-')) fail("bad number");
     return JValue::Int(std::stoll(t_.substr(b, p_ - b)));
   }
+  static constexpr int kMaxDepth = 256;
   const std::string& t_;
   std::size_t p_ = 0;
+  int depth_ = 0;
 };
 
 // ---------------------------------------------------------------- documents

@@ -53,7 +53,7 @@ def _run_ranks(cfg, kind, part, model, tok, watchdog=60.0, only=None):
 
 @pytest.mark.parametrize("kind,P,nv,k,mode", [
     ("seq1f1b", 2, 1, 4, "cwp"), ("seq1f1b", 4, 1, 4, "cwp"), ("1f1b", 4, 1, 1, "even"), ("gpipe", 2, 1, 2, "even"),
-    ("seq1f1b-i", 2, 2, 2, "cwp"), ("1f1b-i", 2, 2, 1, "even"), ("seq1f1b-i", 3, 2, 2, "cwp"),
+    ("seq1f1b-i", 2, 2, 2, "cwp"), ("1f1b-i", 2, 2, 1, "even"), ("seq1f1b-i", 4, 2, 2, "cwp"),
     ("seqzb1p", 4, 1, 4, "even"), ("zb1p", 2, 1, 1, "even")])
 def test_multirank_step_matches_reference_order_and_oracle(gpu, kind, P, nv, k, mode):
     model = _model(layers=2 * P * nv)
@@ -81,6 +81,19 @@ def test_multirank_step_matches_reference_order_and_oracle(gpu, kind, P, nv, k, 
     assert max(bad.values()) < TOL_F32, {n: v for n, v in bad.items() if v >= TOL_F32}
     for e in engines:
         e.close()
+
+
+def test_interleaved_table_the_reference_cannot_complete_is_refused(gpu):
+    """seq1f1b-i at odd P: the reference generate() itself emits an order its own
+    check_schedule flags as order_deadlock (validate.cpp); the engine refuses it up front
+    instead of hanging in a receive."""
+    model = _model(layers=12)
+    cfg = pl.ScenarioConfig(pipeline_size=3, stages_per_device=2, micro_batches=6, segments=2, seq_len=512,
+                            layers=12, hidden_dim=128, param_count=model.param_count())
+    part = pl.cwp_partition(cfg)
+    assert ref.check_schedule(ref.generate(cfg, "seq1f1b-i", part))  # the reference flags its own table
+    with pytest.raises(pl.LogicError, match="order_deadlock"):
+        E.Engine(cfg, "seq1f1b-i", part, model, rank=0, world_size=3, cuda_device=0)
 
 
 def test_multirank_bf16_production_kernels(gpu):

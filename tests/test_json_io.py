@@ -66,6 +66,21 @@ def test_schedule_json_rejects_bad_documents():
             pl.schedule_from_json(bad)
 
 
+def test_schedule_json_parser_bounds_nesting_and_escapes():
+    """User-supplied schedule files (`seqpipe_b200 validate`): deep nesting is an error,
+    not a stack overflow; \\u needs exactly four hex digits; surrogate pairs decode."""
+    err = pl.SeqpipeError if hasattr(pl, "SeqpipeError") else Exception
+    for bad in ("[" * 100000 + "]" * 100000, '{"schema": "\\u12G4"}', '{"schema": "\\ud800"}',
+                '{"schema": "\\udc00x"}', '{"schema": "\\u12"}'):
+        with pytest.raises(err):
+            pl.schedule_from_json(bad)
+    # Within the depth cap and with valid escapes the document parses far enough to fail on schema.
+    for ok_syntax in ("[" * 200 + "]" * 200, '{"schema": "\\ud83d\\ude00"}'):
+        with pytest.raises(err) as e:
+            pl.schedule_from_json(ok_syntax)
+        assert "json parse error" not in str(e.value)
+
+
 def test_bench_config_schedule_and_report_bytes():
     """cfg-2 (GPT-2.7B preset, P 4, M 8, k 4, cwp): schedule and modeled report identical."""
     cfg = pl.preset_scenario("gpt-2.7b")
