@@ -224,4 +224,30 @@ std::vector<Violation> check_warmup_formulas(const Schedule& sch) {  // ref vali
   return out;
 }
 
+// Pairs in device-order position order of the dependent, prerequisites in prereqs() order
+// (the reference's enumeration, validate.cpp:510-528, so seeded picks select the same pairs).
+std::vector<DependencyPair> dependency_order_pairs(const Schedule& sch) {
+  const ScenarioConfig& cfg = sch.config;
+  std::vector<DependencyPair> pairs;
+  for (int d = 1; d <= cfg.pipeline_size && d <= static_cast<int>(sch.device_orders.size()); ++d) {
+    const auto& order = sch.device_orders[static_cast<size_t>(d - 1)];
+    std::map<Key, size_t> at;
+    for (size_t i = 0; i < order.size(); ++i) at[key(order[i])] = i;
+    for (size_t i = 0; i < order.size(); ++i)
+      for (const Task& pre : prereqs(order[i], cfg.segments, cfg.total_stages(), cfg.pipeline_size)) {
+        if (pre.device != d) continue;
+        const auto it = at.find(key(pre));
+        if (it != at.end()) pairs.push_back({d, it->second, i});
+      }
+  }
+  return pairs;
+}
+
+Schedule swap_order_pair(const Schedule& sch, const DependencyPair& pair) {
+  Schedule out = sch;
+  auto& order = out.device_orders.at(static_cast<size_t>(pair.device - 1));
+  std::swap(order.at(pair.prerequisite_index), order.at(pair.dependent_index));
+  return out;
+}
+
 }  // namespace seqpipe
