@@ -304,3 +304,57 @@ def test_bf16_engine_step_at_benchmarked_cfg2_shape(gpu):
     bad = {k: v for k, v in worst.items() if v > TOL_BF16}
     assert not bad, (bad, worst)
     eng.close()
+
+
+def test_bf16_engine_step_at_benchmarked_cfg3_shape(gpu):
+    """One LLaMA-7B-width layer (h 4096, 32 x 128 heads, SwiGLU 11008, RoPE, RMSNorm, vocab 32000)
+    through the engine at the cfg-3 sequence shape bench.py runs (`--workload cfg3-stage`):
+    T = 65536 split by the gpt-7b preset's cwp partition into k = 8 sub-sequences, bf16
+    production kernels (head dim 128: split dK/dV + dQ attention backward), M = 1. Loss and
+    every parameter gradient vs the fp64 oracle (torch backend on the GPU, attention chunked
+    over heads): relative L2 <= 2e-2."""
+    import torch
+    from oracle.transformer import TorchOps
+    bench_cfg = pl.preset_scenario("gpt-7b")
+    for k_, v_ in (("pipeline_size", "8"), ("seq_len", "65536"), ("segments", "8"), ("micro_batches", "2")):
+        pl.apply_scenario_override(bench_cfg, k_, v_)
+    lengths = pl.cwp_partition(bench_cfg).lengths
+    assert sum(lengths) == 65536 and len(lengths) == 8
+    model = E.ModelConfig(family=LLAMA, dtype=E.BF16, vocab=32000, hidden=4096, layers=1, heads=32, head_dim=128,
+                          ffn=11008, max_seq=65536, seed=42)
+    cfg = pl.ScenarioConfig(pipeline_size=1, micro_batches=1, segments=8, seq_len=65536, layers=1, hidden_dim=4096,
+                            param_count=model.param_count())
+    part = pl.make_partition(lengths, cfg)
+    eng = E.Engine(cfg, "seq1f1b", part, model)
+    tok = tokens_for(1, 65536, model.vocab, seed=1234)
+    rep = eng.step(tok)
+    params = {n: eng.read_param(n) for n in eng.params()}
+    grads_eng = {n: eng.read_grad(n) for n in params}
+    eng.close()
+    torch.cuda.empty_cache()
+    oracle = Model(LLAMA, model.vocab, model.hidden, 1, 32, 128, model.ffn, eps=model.norm_eps,
+                   theta=model.rope_theta, ops=TorchOps("cuda"), head_chunk=2)
+    loss, grads = oracle.step(params, tok, lengths)
+    del oracle
+    torch.cuda.empty_cache()
+    assert abs(rep.loss - loss) / abs(loss) < TOL_BF16, (rep.loss, loss)
+    worst = {n: rel_l2(grads_eng[n], grads[n]) for n in params}
+    bad = {k: v for k, v in worst.items() if v > TOL_BF16}
+    assert not bad, (bad, worst)
+
+
+def test_llama_stage_loss_decreases_like_memorisation_not_copying(gpu):
+    """Five AdamW steps of a 2-layer LLaMA at T = 8192 (k = 4) on one fixed batch of uniform
+    random tokens: a causal model can only memorise, so the loss must stay within a few nats of
+    ln(V) -- a drop towards 0 would mean a query saw its own target (a causal-mask leak)."""
+    import math
+    model = E.ModelConfig(family=LLAMA, dtype=E.BF16, vocab=4096, hidden=1024, layers=2, heads=8, head_dim=128,
+                          ffn=2816, max_seq=8192, seed=42, lr=1e-4, weight_decay=0.0)
+    cfg = pl.ScenarioConfig(pipeline_size=1, micro_batches=2, segments=4, seq_len=8192, layers=2, hidden_dim=1024,
+                            param_count=model.param_count())
+    eng = E.Engine(cfg, "seq1f1b", pl.cwp_partition(cfg), model)
+    tok = tokens_for(2, 8192, model.vocab, seed=3)
+    losses = [eng.step(tok).loss for _ in range(5)]
+    eng.close()
+    assert abs(losses[0] - math.log(4096)) < 0.5, losses
+    assert losses[-1] > 0.5 * math.log(4096), losses

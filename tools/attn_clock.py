@@ -1,6 +1,8 @@
 #!/usr/bin/env python
 """SM clock / power / throttle reasons while the attention kernels run back to back:
-attn_clock.py [fwd|bwd] [n q_off H hd]. Prints ms per call and the median SM clock."""
+attn_clock.py [fwd|bwd|bwd-split] [n q_off H hd]. Prints ms per call, algorithmic TFLOP/s
+(fwd 4*H*hd*(n*q_off + n^2/2), bwd twice that) and the median SM clock. bwd = the default
+backward (fused at hd <= 80), bwd-split = the split dK/dV + dQ-recompute kernels (impl 3)."""
 import ctypes as C
 import sys
 import threading
@@ -30,8 +32,11 @@ def fwd():
     _capi.check(lib.sp_attention_fwd(1, 0, P(q), P(kv), P(o), P(lse), n, q_off, L, H, hd, C.c_void_p(s)))
 
 
+BWD_IMPL = 3 if which == "bwd-split" else 0
+
+
 def bwd():
-    _capi.check(lib.sp_attention_bwd(1, 0, P(q), P(kv), P(o), P(dout), P(lse), P(dq), P(dkv), n, q_off, L, H, hd,
+    _capi.check(lib.sp_attention_bwd(1, BWD_IMPL, P(q), P(kv), P(o), P(dout), P(lse), P(dq), P(dkv), n, q_off, L, H, hd,
                                      C.c_void_p(s)))
 
 
@@ -68,5 +73,7 @@ pw = sorted(x[1] for x in samples)
 reasons = 0
 for x in samples:
     reasons |= x[2]
-print(f"{which}: {e0.elapsed_time(e1) / reps:.3f} ms/call  sm_mhz median {clk[len(clk) // 2]} "
+ms = e0.elapsed_time(e1) / reps
+fl = 4 * H * hd * (n * q_off + n * n / 2) * (1 if which == "fwd" else 2)
+print(f"{which}: {ms:.3f} ms/call  {fl / ms / 1e9:.0f} TF algorithmic  sm_mhz median {clk[len(clk) // 2]} "
       f"(min {clk[0]} max {clk[-1]})  power median {pw[len(pw) // 2]:.0f} W  reasons 0x{reasons:x}")

@@ -75,6 +75,16 @@ __global__ void __launch_bounds__(384, 1) mma_bench(int iters, unsigned long lon
       if (KIND == 8) tc::mma_bf16_ts_w(tmem + 256, tmem, bd, tc::idesc_bf16(128, 32, false, false), 1);
       if (KIND == 9) tc::mma_bf16_ts_w(tmem + 256, tmem, bd, tc::idesc_bf16(128, 16, false, false), 1);
       if (KIND == 10) tc::mma_bf16_ss_w(tmem + 256, ad, bd, tc::idesc_bf16(128, 32, false, false), 1);
+      // fused-backward dQ^T = K^T dS^T shapes: B = dS^T tile, MN-major (N = queries)
+      if (KIND == 14)
+        tc::mma_bf16_ts_w(tmem + 256, tmem, tc::smem_desc(b + (i & 7) * 1024, 4096, 512, tc::kSwizzle64B),
+                          tc::idesc_bf16(128, 32, false, true), 1);
+      if (KIND == 15)
+        tc::mma_bf16_ts_w(tmem + 256, tmem, tc::smem_desc(b + (i & 7) * 2048, 8192, 1024, tc::kSwizzle128B),
+                          tc::idesc_bf16(128, 64, false, true), 1);
+      if (KIND == 16)  // dV / dK of a 32-query block: N = 80, B MN-major 32-row tile
+        tc::mma_bf16_ts_w(tmem + 256, tmem, tc::smem_desc(b + (i & 1) * 2048, 4096, 1024, tc::kSwizzle128B),
+                          tc::idesc_bf16(128, 80, false, true), 1);
       if (KIND == 11) {  // wait-free group: 5 MMAs + commit + a TRYWAIT on an already-complete barrier
         for (int kk = 0; kk < 5; ++kk) tc::mma_bf16_ts_w(tmem + 256, tmem + 8 * kk, bd, tc::idesc_bf16(128, 64, false, false), 1);
         tc::mma_commit_w(&bar2[0]);
@@ -139,16 +149,19 @@ int main() {
   const char* names[] = {"SS 128x64x16", "TS 128x80x16 (A tmem, B MN-major)", "SS 128x128x16", "SS 128x256x16",
                          "TS 128x256x16", "dKV iteration (18 TS MMAs)", "dKV iteration + 3 commits", "TS 128x64x16",
                          "TS 128x32x16", "TS 128x16x16", "SS 128x32x16", "5xTS N64 + commit + completed wait",
-                         "dKV iteration + 8 warps tcgen05.ld", "dKV iteration + 8 warps ld+st"};
+                         "dKV iteration + 8 warps tcgen05.ld", "dKV iteration + 8 warps ld+st",
+                         "TS 128x32x16 B MN-major SW64", "TS 128x64x16 B MN-major SW128", "TS 128x80x16 B MN 32-row"};
   const double fma[] = {128 * 64 * 16, 128 * 80 * 16, 128 * 128 * 16, 128 * 256 * 16, 128 * 256 * 16,
                         4.0 * 128 * 64 * 80, 4.0 * 128 * 64 * 80, 128 * 64 * 16, 128 * 32 * 16, 128 * 16 * 16,
-                        128 * 32 * 16, 5.0 * 128 * 64 * 16, 4.0 * 128 * 64 * 80, 4.0 * 128 * 64 * 80};
-  for (int k = 0; k < 14; ++k) {
+                        128 * 32 * 16, 5.0 * 128 * 64 * 16, 4.0 * 128 * 64 * 80, 4.0 * 128 * 64 * 80,
+                        128 * 32 * 16, 128 * 64 * 16, 128 * 80 * 16};
+  for (int k = 0; k < 17; ++k) {
     void (*f)(int, unsigned long long*) = k == 0 ? mma_bench<0> : k == 1 ? mma_bench<1> : k == 2 ? mma_bench<2>
                                           : k == 3 ? mma_bench<3> : k == 4 ? mma_bench<4> : k == 5 ? mma_bench<5>
                                           : k == 6 ? mma_bench<6> : k == 7 ? mma_bench<7> : k == 8 ? mma_bench<8>
                                           : k == 9 ? mma_bench<9> : k == 10 ? mma_bench<10> : k == 11 ? mma_bench<11>
-                                          : k == 12 ? mma_bench<12> : mma_bench<13>;
+                                          : k == 12 ? mma_bench<12> : k == 13 ? mma_bench<13>
+                                          : k == 14 ? mma_bench<14> : k == 15 ? mma_bench<15> : mma_bench<16>;
     const bool grp = k == 5 || k == 6 || k == 11 || k == 12 || k == 13;
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000);
     f<<<148, 384, 140000>>>(grp ? iters / 8 : iters, d);
