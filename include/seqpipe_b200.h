@@ -375,9 +375,7 @@ int sp_gemm(int32_t dtype, int32_t impl, const void* A, int32_t a_kmajor, const 
 int sp_attention_fwd(int32_t dtype, int32_t impl, const void* q, const void* kv, void* o, float* lse,
                      int64_t n, int64_t q_off, int64_t kv_len, int32_t heads, int32_t head_dim,
                      void* stream);
-/* dq [n, H*hd] (dtype), dkv_acc [kv_len, 2*H*hd] fp32 accumulated (+=). impl: 0 auto (bf16:
- * tensor cores; head dim <= 80 runs the fused dK/dV/dQ kernel), 1 SIMT, 2 tensor cores,
- * 3 tensor cores through the split dK/dV + dQ-recompute kernels (the head-dim-128 path). */
+/* dq [n, H*hd] (dtype), dkv_acc [kv_len, 2*H*hd] fp32 accumulated (+=). */
 int sp_attention_bwd(int32_t dtype, int32_t impl, const void* q, const void* kv, const void* o,
                      const void* dout, const float* lse, void* dq, float* dkv_acc, int64_t n,
                      int64_t q_off, int64_t kv_len, int32_t heads, int32_t head_dim, void* stream);

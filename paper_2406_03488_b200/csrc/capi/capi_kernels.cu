@@ -71,7 +71,7 @@ int sp_attention_bwd(int32_t dtype, int32_t impl, const void* q, const void* kv,
     static thread_local size_t ws_cap[64] = {};
     int dev = 0;
     SPK_CUDA(cudaGetDevice(&dev));
-    const size_t floats = spk::attn_bwd_ws_delta_floats(n, heads) + spk::attn_bwd_ws_dq_floats(n, heads, head_dim);
+    const size_t floats = spk::attn_bwd_ws_delta_floats(n, heads) + static_cast<size_t>(n) * heads * head_dim;
     if (dev < 0 || dev >= 64) throw std::invalid_argument("device ordinal out of range");
     if (ws_cap[dev] < floats) {
       if (ws_buf[dev]) SPK_CUDA(cudaFree(ws_buf[dev]));

@@ -15,9 +15,9 @@ void attn_bwd_simt(DType t, const void* q, const void* kv, const void* o, const 
 bool attn_tc_supported(DType t, int hd);
 void attn_fwd_tc(const void* q, const void* kv, void* o, float* lse, int64_t n, int64_t q_off, int64_t kv_len, int H,
                  int hd, cudaStream_t s);
-void attn_bwd_tc(bool dkv_overwrite, bool split, const void* q, const void* kv, const void* o, const void* dout,
-                 const float* lse, float* ws_delta, float* ws_dq, void* dq, float* dkv, int64_t n, int64_t q_off,
-                 int64_t kv_len, int H, int hd, cudaStream_t s);
+void attn_bwd_tc(bool dkv_overwrite, const void* q, const void* kv, const void* o, const void* dout, const float* lse, float* ws_delta,
+                 float* ws_dq, void* dq, float* dkv, int64_t n, int64_t q_off, int64_t kv_len, int H, int hd,
+                 cudaStream_t s);
 
 void attn_fwd(DType t, int impl, const void* q, const void* kv, void* o, float* lse, int64_t n, int64_t q_off,
               int64_t kv_len, int H, int hd, cudaStream_t s) {
@@ -39,13 +39,11 @@ void attn_bwd(DType t, int impl, const void* q, const void* kv, const void* o, c
   if (n == 0) return;
   if (kv_len != q_off + n) throw std::invalid_argument("attention: kv_len must equal q_off + n (causal prefix)");
   const bool tc = impl != kAttnSimt && t == DType::kBF16;
-  if ((impl == kAttnTensor || impl == kAttnTensorSplit) && t != DType::kBF16)
-    throw std::invalid_argument("attention: tensor-core path needs bf16");
+  if (impl == kAttnTensor && t != DType::kBF16) throw std::invalid_argument("attention: tensor-core path needs bf16");
   if (tc && !attn_tc_supported(t, hd))
     throw std::invalid_argument("attention: bf16 tensor-core kernels support head_dim 64, 80, 128 (no SIMT fallback)");
   if (tc) {
-    attn_bwd_tc(dkv_overwrite, impl == kAttnTensorSplit, q, kv, o, dout, lse, ws_delta, ws_dq, dq, dkv, n, q_off, kv_len,
-                H, hd, s);
+    attn_bwd_tc(dkv_overwrite, q, kv, o, dout, lse, ws_delta, ws_dq, dq, dkv, n, q_off, kv_len, H, hd, s);
   } else {
     if (dkv_overwrite)
       SPK_CUDA(cudaMemsetAsync(dkv, 0, sizeof(float) * static_cast<size_t>(kv_len) * 2 * H * hd, s));

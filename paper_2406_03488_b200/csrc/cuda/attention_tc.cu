@@ -24,7 +24,6 @@
 // both deterministic, no atomics.
 #include <cudaTypedefs.h>
 
-#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -125,11 +124,6 @@ struct __align__(64) AttnParams {
 };
 
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -603,7 +597,6 @@ struct __align__(64) AttnBwdParams {
   float* dkv;        // [kv_len, 2h] fp32 accumulator
   int dkv_store;     // dK/dV epilogue writes (TMA store) instead of adding (first op of a micro-batch)
   __nv_bfloat16* dq; // [n, h]
-  float* dq_acc;     // fused kernel: [n_pad, h] fp32 accumulator of dS K (unscaled), zeroed by the host
   int64_t n, q_off, kv_len;
   int H, h;
   float scale, scale_log2;
@@ -679,69 +672,6 @@ __device__ __forceinline__ void trace_mark(const AttnBwdParams& p, int ev, int i
   if constexpr (!SPK_ATTN_PROFILING) return;
   // every lane stores the same stamp: no lane-divergent branch in the MMA warp
   if (p.trace && it < 64 && blockIdx.x == gridDim.x - 1 && blockIdx.y == 0) p.trace[ev * 64 + it] = clock64();
-}
-
-// dK/dV epilogue (softmax warps of a dK/dV or fused backward CTA, after every MMA
-// completed): dK (scaled) / dV rows -> SMEM [2][128][HD] fp32 (the Q/dO ring is
-// idle), then one thread adds both tiles into the fp32 accumulator with TMA
-// reduce-add (coalesced, asynchronous in L2; rows >= kv_len are clipped by the
-// map), or stores them for the first backward op of a micro-batch.
-template <int HD>
-__device__ __forceinline__ void dkv_epilogue(const AttnBwdParams& p, uint8_t* sm, uint32_t tmem, uint32_t lane_base,
-                                             uint32_t t_dv, uint32_t t_dk, int r, int g, int warp, int lane, int64_t j0,
-                                             int head) {
-  float* out = reinterpret_cast<float*>(sm);
-  constexpr int NCH = HD / 16;
-  for (int t = g; t < 2 * NCH; t += 4) {  // 16-column chunks of dV (t < NCH) then dK
-    const bool is_k = t >= NCH;
-    const int c = is_k ? t - NCH : t;
-    uint32_t v[16];
-    tmem_ld16(tmem + lane_base + (is_k ? t_dk : t_dv) + c * 16, v);
-    tc::tmem_ld_wait();
-    const float sc = is_k ? p.scale : 1.f;
-    // staging = the reduce boxes: 32-column [128 x 128 B] tiles (128-byte swizzle) and,
-    // for head dim 80, a 16-column [128 x 64 B] tile (64-byte swizzle): the per-row
-    // float4 stores are bank-conflict free (a dense [128 x HD] tile is 16-way).
-    uint8_t* tile = reinterpret_cast<uint8_t*>(out + (is_k ? 0 : 128 * HD));
-#pragma unroll
-    for (int e = 0; e < 16; e += 4) {
-      uint8_t* dst;
-      if (c < 2 * (HD / 32)) {
-        const int u = (c & 1) * 4 + e / 4;
-        dst = tile + (c >> 1) * 16384 + r * 128 + ((u ^ (r & 7)) << 4);
-      } else {
-        const int u = e / 4;
-        dst = tile + (HD / 32) * 16384 + r * 64 + ((u ^ ((r >> 1) & 3)) << 4);
-      }
-      *reinterpret_cast<float4*>(dst) =
-          make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
-                      __uint_as_float(v[e + 3]) * sc);
-    }
-  }
-  tc::fence_proxy_async_smem();
-  tc::named_bar_sync(1, 512);
-  if (warp == 4 && lane == 0) {
-#pragma unroll
-    for (int is_v = 0; is_v < 2; ++is_v) {
-      const float* tile = out + is_v * 128 * HD;
-      const int col = (is_v ? p.h : 0) + head * HD;
-#pragma unroll
-      for (int b = 0; b < HD / 32; ++b) {
-        if (p.dkv_store)
-          tc::tma_store_2d(&p.tdkv32, tile + b * 4096, col + 32 * b, static_cast<int>(j0));
-        else
-          tc::tma_reduce_add_2d(&p.tdkv32, tile + b * 4096, col + 32 * b, static_cast<int>(j0));
-      }
-      if constexpr (HD % 32 == 16) {
-        if (p.dkv_store)
-          tc::tma_store_2d(&p.tdkv16, tile + (HD / 32) * 4096, col + HD - 16, static_cast<int>(j0));
-        else
-          tc::tma_reduce_add_2d(&p.tdkv16, tile + (HD / 32) * 4096, col + HD - 16, static_cast<int>(j0));
-      }
-    }
-    tc::bulk_commit();
-    tc::bulk_wait_read0();  // SMEM must outlive the copy-out
-  }
 }
 
 // dK/dV: one CTA per (128-key block, head), looping over 64-query blocks that
@@ -1000,360 +930,68 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
     tc::mbar_wait(done, 0);
     tc::tc_fence_after();
     if (warp == 4) trace_mark(p, 8, 0);
-    dkv_epilogue<HD>(p, sm, tmem, lane_base, C::T_DV, C::T_DK, r, g, warp, lane, j0, head);
+    // Epilogue: dK (scaled) / dV rows -> SMEM [2][128][HD] fp32 (the Q/dO ring is
+    // idle: every MMA completed and every multicast stage was consumed), then one
+    // thread adds both tiles into the fp32 accumulator with TMA reduce-add
+    // (coalesced, asynchronous in L2; rows >= kv_len are clipped by the map).
+    float* out = reinterpret_cast<float*>(sm);
+    constexpr int NCH = HD / 16;
+    for (int t = g; t < 2 * NCH; t += 4) {  // 16-column chunks of dV (t < NCH) then dK
+      const bool is_k = t >= NCH;
+      const int c = is_k ? t - NCH : t;
+      uint32_t v[16];
+      tmem_ld16(tmem + lane_base + (is_k ? C::T_DK : C::T_DV) + c * 16, v);
+      tc::tmem_ld_wait();
+      const float sc = is_k ? p.scale : 1.f;
+      // staging = the reduce boxes: 32-column [128 x 128 B] tiles (128-byte swizzle) and,
+      // for head dim 80, a 16-column [128 x 64 B] tile (64-byte swizzle): the per-row
+      // float4 stores are bank-conflict free (a dense [128 x HD] tile is 16-way).
+      uint8_t* tile = reinterpret_cast<uint8_t*>(out + (is_k ? 0 : 128 * HD));
+#pragma unroll
+      for (int e = 0; e < 16; e += 4) {
+        uint8_t* dst;
+        if (c < 2 * (HD / 32)) {
+          const int u = (c & 1) * 4 + e / 4;
+          dst = tile + (c >> 1) * 16384 + r * 128 + ((u ^ (r & 7)) << 4);
+        } else {
+          const int u = e / 4;
+          dst = tile + (HD / 32) * 16384 + r * 64 + ((u ^ ((r >> 1) & 3)) << 4);
+        }
+        *reinterpret_cast<float4*>(dst) =
+            make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
+                        __uint_as_float(v[e + 3]) * sc);
+      }
+    }
+    tc::fence_proxy_async_smem();
+    tc::named_bar_sync(1, 512);
+    if (warp == 4 && lane == 0) {
+#pragma unroll
+      for (int is_v = 0; is_v < 2; ++is_v) {
+        const float* tile = out + is_v * 128 * HD;
+        const int col = (is_v ? p.h : 0) + head * HD;
+#pragma unroll
+        for (int b = 0; b < HD / 32; ++b) {
+          if (p.dkv_store)
+            tc::tma_store_2d(&p.tdkv32, tile + b * 4096, col + 32 * b, static_cast<int>(j0));
+          else
+            tc::tma_reduce_add_2d(&p.tdkv32, tile + b * 4096, col + 32 * b, static_cast<int>(j0));
+        }
+        if constexpr (HD % 32 == 16) {
+          if (p.dkv_store)
+            tc::tma_store_2d(&p.tdkv16, tile + (HD / 32) * 4096, col + HD - 16, static_cast<int>(j0));
+          else
+            tc::tma_reduce_add_2d(&p.tdkv16, tile + (HD / 32) * 4096, col + HD - 16, static_cast<int>(j0));
+        }
+      }
+      tc::bulk_commit();
+      tc::bulk_wait_read0();  // SMEM must outlive the copy-out
+    }
     if (warp == 4) trace_mark(p, 9, 0);
   }
   tc::tc_fence_before();
   tc::cluster_sync();  // no multicast data / remote arrive may target an exited CTA
   tc::tc_fence_after();
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
-}
-
-// ---------------------------------------------------------------- fused backward (hd <= 80)
-// One CTA per (128-key block, head) and 2-CTA clusters sharing multicast Q / dO
-// tiles, as in the dK/dV kernel, but dQ comes out of the same pass -- no dQ
-// kernel re-computing S and dP (7 -> 5 GEMM-equivalents per block, half the
-// exponentials). Per 32-query block i:
-//   S^T_i = K Q_i^T, dP^T_i = V dO_i^T        (TS: K, V copied into TMEM)
-//   softmax warps: P^T = exp2(S^T c - LSE), dS^T = P^T (dP^T - delta), packed
-//     bf16 into the dP buffer (P^T | dS^T) and dS^T also into SMEM
-//   dV += P^T dO_i, dK += dS^T Q_i            (TS: A from TMEM)
-//   dQ^T_i = K^T dS^T_i                        (TS: A = K^T in TMEM, lanes = head
-//     dims, zero beyond hd; B = the SMEM dS^T tile, MN-major)
-// Every TMEM buffer the loop writes is double-buffered (S^T, dP^T, dQ^T) and so
-// is the SMEM dS^T tile, so S^T / dP^T of block i+1 run while the softmax works
-// on block i, and dV / dK / dQ^T of block i while it works on block i+1. The
-// softmax warps drain dQ^T_{i-1} from TMEM into an fp32 [n_pad, h] accumulator
-// with coalesced red.global.add (one instruction = 32 consecutive head dims of
-// one query row); the host scales it into bf16 dQ.
-// TMEM (512 columns):
-//   S^T 2x32 | dP^T 2x32 | dQ^T 2x32 | dV 96 | dK hd | K hd/2 | V hd/2 | K^T 64
-constexpr int FBQ = 32;  // queries per block
-template <int HD>
-struct FusedCfg {
-  static constexpr uint32_t T_S = 0, T_DP = 64, T_DQ = 128, T_DV = 192, T_DK = T_DV + 96;
-  static constexpr uint32_t T_K = T_DK + HD, T_V = T_K + HD / 2, T_KT = T_V + HD / 2;
-  static_assert(HD <= 80, "fused backward keeps K and V in TMEM (hd <= 80)");
-  static_assert(T_KT + 64 <= 512, "fused backward TMEM budget");
-};
-constexpr int kDsBytes = 128 * FBQ * 2;  // dS^T tile [128 keys x 32 queries] bf16: 64-byte rows, 64-byte swizzle
-
-template <int HD>
-constexpr size_t fused_smem_n(int st) {
-  return 2 * kDsBytes + 2 * st * Lay<HD>::bytes(FBQ) + st * 256 + (24 + 2 * st) * 8 + 8 + 1024;
-}
-template <int HD>
-constexpr int fused_stages() {
-  int st = 8;
-  while (fused_smem_n<HD>(st) > 232448) --st;
-  return st;
-}
-template <int HD>
-constexpr size_t fused_smem() {
-  return fused_smem_n<HD>(fused_stages<HD>());
-}
-
-template <int HD>
-__global__ void __launch_bounds__(640, 1) attn_bwd_fused_k(const __grid_constant__ AttnBwdParams p) {
-  using C = FusedCfg<HD>;
-  constexpr int QST = fused_stages<HD>();
-  constexpr int Q_T = Lay<HD>::bytes(FBQ);
-  static_assert(2 * 128 * HD * 4 <= QST * 2 * Q_T, "dK/dV epilogue staging must fit the ring");
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;                                           // [QST]
-  uint8_t* sdO = sQ + QST * Q_T;                              // [QST]
-  uint8_t* sDS = sdO + QST * Q_T;                             // [2] dS^T tiles (1024-aligned)
-  float* sLD = reinterpret_cast<float*>(sDS + 2 * kDsBytes);  // [QST][-LSE*log2e x 32, -delta x 32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + QST * 64);
-  uint64_t* kv_full = bars;        // K, V, K^T copied into TMEM (16 softmax warps)
-  uint64_t* done = bars + 1;       // last dV/dK completed
-  uint64_t* s_full = bars + 2;     // [2] S^T_i landed
-  uint64_t* s_free = bars + 4;     // [2] S^T_i loaded by the softmax (16 warps)
-  uint64_t* dp_full = bars + 6;    // [2] dP^T_i landed
-  uint64_t* sm_done = bars + 8;    // [2] P^T_i | dS^T_i packed, dS^T_i in SMEM (16 warps)
-  uint64_t* dpb_free = bars + 10;  // [2] dV/dK_i completed: dP buffer i % 2 reusable
-  uint64_t* dq_full = bars + 12;   // [2] dQ^T_i landed
-  uint64_t* dq_free = bars + 14;   // [2] dQ^T_i drained by the softmax warps (16 warps)
-  uint64_t* ds_free = bars + 16;   // [2] dQ^T_i completed: dS^T tile i % 2 reusable
-  uint64_t* q_full = bars + 24;          // [QST]
-  uint64_t* q_empty = q_full + QST;      // [QST]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + QST);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = tc::cluster_ctarank();
-  const int num_kb = static_cast<int>((p.kv_len + 127) / 128);
-  const int num_kb2 = (num_kb + 1) & ~1;
-  const int kb = num_kb2 - 1 - static_cast<int>(blockIdx.x);  // may be == num_kb (idle keys)
-  const int head = blockIdx.y;
-  const int64_t j0 = static_cast<int64_t>(kb) * 128;
-  const int64_t j0_lo = static_cast<int64_t>(num_kb2 - 2 - 2 * static_cast<int>(blockIdx.x / 2)) * 128;
-  int64_t ib0 = j0_lo - p.q_off;  // first query block any key of the pair can see (common to the cluster)
-  if (ib0 < 0) ib0 = 0;
-  ib0 = ib0 / 64 * 64;  // the (LSE, delta) workspace is laid out in 64-query blocks
-  const int niter = static_cast<int>((p.n - ib0 + FBQ - 1) / FBQ);
-
-  if (threadIdx.x == 0) {
-    tc::mbar_init(kv_full, 16);
-    tc::mbar_init(done, 1);
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&s_full[b], 1);
-      tc::mbar_init(&s_free[b], 8);
-      tc::mbar_init(&dp_full[b], 1);
-      tc::mbar_init(&sm_done[b], 8);
-      tc::mbar_init(&dpb_free[b], 1);
-      tc::mbar_init(&dq_full[b], 1);
-      tc::mbar_init(&dq_free[b], 8);
-      tc::mbar_init(&ds_free[b], 1);
-    }
-    for (int i = 0; i < QST; ++i) {
-      tc::mbar_init(&q_full[i], 1);
-      tc::mbar_init(&q_empty[i], 2);  // freed by both CTAs' MMA commits
-    }
-    tc::fence_mbar_init();
-  }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
-  tc::tc_fence_before();
-  tc::cluster_sync();
-  tc::tc_fence_after();
-  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-
-  if (warp == 0) {
-    if (lane == 0) {
-      tc::tma_prefetch(&p.tq.m0);
-      tc::tma_prefetch(&p.tdo.m0);
-      for (int it = 0; it < niter; ++it) {
-        const int st = it % QST;
-        const int64_t i0 = ib0 + static_cast<int64_t>(it) * FBQ;
-        tc::mbar_wait(&q_empty[st], ((it / QST) & 1) ^ 1);  // stage free in both CTAs
-        trace_mark(p, 0, it);
-        tc::mbar_expect_tx(&q_full[st], 2 * Q_T + 256);
-        if (rank == 0)
-          load_tile<HD>(sQ + st * Q_T, p.tq, &q_full[st], head * HD, static_cast<int>(i0), FBQ, 3);
-        else
-          load_tile<HD>(sdO + st * Q_T, p.tdo, &q_full[st], head * HD, static_cast<int>(i0), FBQ, 3);
-        // (-LSE*log2e, -delta) of the 32 queries: two 128-byte bulk copies from the 64-query layout
-        const float* ld = p.ld + (static_cast<int64_t>(head) * p.n_pad + (i0 & ~int64_t(63))) * 2 + (i0 & 63);
-        tc::bulk_load(sLD + st * 64, ld, 128, &q_full[st]);
-        tc::bulk_load(sLD + st * 64 + 32, ld + 64, 128, &q_full[st]);
-      }
-    }
-  } else if (warp >= 1 && warp <= 3) {
-    // MMA-issuing warps (converged; tc::*_w elect the issuing lane), one MMA stream each:
-    //   warp 3: S^T_i once the softmax loaded S^T_{i-2} (buffer i % 2);
-    //   warp 1: dP^T_i once dV/dK_{i-2} released dP buffer i % 2;
-    //   warp 2: dV/dK_i and dQ^T_i once the softmax packed block i.
-    constexpr uint32_t idesc_s = tc::idesc_bf16(128, FBQ, false, false);
-    constexpr uint32_t idesc_dq = tc::idesc_bf16(128, FBQ, false, true);
-    tc::mbar_wait_w(kv_full, 0);
-    tc::tc_fence_after();
-    auto kv_mma = [&](uint32_t d, uint32_t t_a, uint32_t b_base) {
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk)
-        tc::mma_bf16_ts_w(d, tmem + t_a + 8 * kk, kdesc<HD>(b_base, FBQ, kk), idesc_s, kk > 0);
-    };
-    if (warp == 1) {
-      for (int it = 0; it < niter; ++it) {
-        const int st = it % QST, b = it & 1;
-        tc::mbar_wait_w(&q_full[st], (it / QST) & 1);
-        if (it >= 2) tc::mbar_wait_w(&dpb_free[b], ((it >> 1) - 1) & 1);
-        tc::tc_fence_after();
-        kv_mma(tmem + C::T_DP + 32 * b, C::T_V, tc::smem_u32(sdO + st * Q_T));
-        tc::mma_commit_w(&dp_full[b]);
-        trace_mark(p, 2, it);
-      }
-    } else if (warp == 3) {
-      for (int it = 0; it < niter; ++it) {
-        const int st = it % QST, b = it & 1;
-        tc::mbar_wait_w(&q_full[st], (it / QST) & 1);
-        if (it >= 2) tc::mbar_wait_w(&s_free[b], ((it >> 1) - 1) & 1);
-        tc::tc_fence_after();
-        kv_mma(tmem + C::T_S + 32 * b, C::T_K, tc::smem_u32(sQ + st * Q_T));
-        tc::mma_commit_w(&s_full[b]);
-        trace_mark(p, 3, it);
-      }
-    } else {
-      for (int it = 0; it < niter; ++it) {
-        const int st = it % QST, b = it & 1;
-        tc::mbar_wait_w(&sm_done[b], (it >> 1) & 1);
-        trace_mark(p, 15, it);
-        tc::tc_fence_after();
-        const uint32_t q_base = tc::smem_u32(sQ + st * Q_T), do_base = tc::smem_u32(sdO + st * Q_T);
-        const uint32_t pcol = C::T_DP + 32 * b;  // queries [16kk, 16kk+16): P^T at pcol+16kk, dS^T at +8
-#pragma unroll
-        for (int kk = 0; kk < FBQ / 16; ++kk) {
-          const bool acc = it > 0 || kk > 0;
-          mma_nhd_ts<HD>(tmem + C::T_DV, tmem + pcol + 16 * kk, do_base, FBQ, kk, acc);
-          mma_nhd_ts<HD>(tmem + C::T_DK, tmem + pcol + 16 * kk + 8, q_base, FBQ, kk, acc);
-        }
-        tc::mma_commit_mc_w(&q_empty[st], 3);  // this CTA is done with the multicast stage
-        tc::mma_commit_w(&dpb_free[b]);
-        trace_mark(p, 1, it);
-        // dQ^T_i = K^T dS^T_i (K = 128 keys) into dQ buffer i % 2 once dQ^T_{i-2} was drained
-        if (it >= 2) tc::mbar_wait_w(&dq_free[b], ((it >> 1) - 1) & 1);
-        tc::tc_fence_after();
-        const uint32_t ds_base = tc::smem_u32(sDS + b * kDsBytes);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          if (!(prof_dbg(p) & 8))
-            tc::mma_bf16_ts_w(tmem + C::T_DQ + 32 * b, tmem + C::T_KT + 8 * kk,
-                              tc::smem_desc(ds_base + kk * 1024, 4096, 512, tc::kSwizzle64B), idesc_dq, kk > 0);
-        tc::mma_commit_w(&dq_full[b]);
-        tc::mma_commit_w(&ds_free[b]);
-        trace_mark(p, 10, it);
-      }
-      tc::mma_commit_w(done);
-    }
-  } else if (warp >= 4) {
-    // 16 softmax warps in two groups of 8: group G = (w-4)/8 takes the blocks i with
-    // i % 2 == G (and with them TMEM / SMEM buffer G), so one group's barrier and TMEM
-    // latencies overlap the other group's exponentials. Within a group, warp (half,
-    // quarter) owns TMEM lane quarter w%4 (a key row per lane for S^T / dP^T, a head
-    // dim per lane for dQ^T) and query columns [16 half, 16 half + 16) of the block; it
-    // writes P^T | dS^T back into exactly the dP columns it read.
-    const int quarter = warp & 3, g = (warp - 4) >> 2, grp = g >> 1, half = g & 1;
-    const int r = quarter * 32 + lane;  // key row (S^T, dP^T) / head dim (dQ^T)
-    const int64_t kpos = j0 + r;
-    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    {
-      const bool kv_ok = kpos < p.kv_len;
-      const int part = g & 1;
-      row_part_to_tmem<HD>(tmem + lane_base + (g >= 2 ? C::T_V : C::T_K) + part * (HD / 4),
-                           p.kv + (kv_ok ? kpos : 0) * 2 * p.h + (g >= 2 ? p.h : 0) + head * HD + part * (HD / 2),
-                           kv_ok);
-      // K^T: lane = head dim r, columns [16g, 16g+16) = keys [32g, 32g+32) as bf16 pairs
-      uint32_t kt[16];
-      const bool d_ok = r < HD;
-      const __nv_bfloat16* kcol = p.kv + head * HD + (d_ok ? r : 0);
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const int64_t k0 = j0 + 32 * g + 2 * c;
-        const __nv_bfloat16 zero = __float2bfloat16(0.f);
-        const __nv_bfloat16 a = (d_ok && k0 < p.kv_len) ? kcol[k0 * 2 * p.h] : zero;
-        const __nv_bfloat16 b = (d_ok && k0 + 1 < p.kv_len) ? kcol[(k0 + 1) * 2 * p.h] : zero;
-        kt[c] = static_cast<uint32_t>(__bfloat16_as_ushort(a)) | (static_cast<uint32_t>(__bfloat16_as_ushort(b)) << 16);
-      }
-      tc::tmem_st16(tmem + lane_base + C::T_KT + 16 * g, kt);
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      warp_arrive(kv_full);
-    }
-    // dQ^T_i drain (block i of this group): this warp's 16 query columns of head dims r (< HD)
-    // -> the fp32 accumulator.
-    auto drain_dq = [&](int i) {
-      tc::mbar_wait(&dq_full[grp], (i >> 1) & 1);
-      if (warp == 4 || warp == 12) trace_mark(p, 8, i);
-      tc::tc_fence_after();
-      uint32_t v[16];
-      tmem_ld16(tmem + lane_base + C::T_DQ + 32 * grp + 16 * half, v);
-      tc::tmem_ld_wait();
-      tc::tc_fence_before();
-      warp_arrive(&dq_free[grp]);
-      if (r < HD && !(prof_dbg(p) & 4)) {
-        float* dst = p.dq_acc + (ib0 + static_cast<int64_t>(i) * FBQ + 16 * half) * p.h + head * HD + r;
-#pragma unroll
-        for (int c = 0; c < 16; ++c)
-          asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + static_cast<int64_t>(c) * p.h), "f"(__uint_as_float(v[c]))
-                       : "memory");
-      }
-      if (warp == 4 || warp == 12) trace_mark(p, 9, i);
-    };
-    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-    for (int it = grp; it < niter; it += 2) {
-      const int st = it % QST;
-      const int64_t i0 = ib0 + static_cast<int64_t>(it) * FBQ;
-      const float* nl = sLD + st * 64 + half * 16;  // -LSE*log2e of this warp's 16 queries
-      const float* nd = nl + 32;                    // -delta of the same queries
-      const int64_t cbase = i0 + half * 16;
-      const int64_t cmin = kpos - p.q_off - cbase;
-      const int c_lo = cmin < 0 ? 0 : (cmin > 16 ? 16 : static_cast<int>(cmin));
-      const int64_t chi = p.n - cbase;
-      const int c_hi = chi < 0 ? 0 : (chi > 16 ? 16 : static_cast<int>(chi));  // exclusive
-      const bool full_blk = __all_sync(0xffffffffu, c_lo == 0 && c_hi == 16);
-      tc::mbar_wait(&q_full[st], (it / QST) & 1);  // LSE / delta of this block are in SMEM
-      if (warp == 4 || warp == 12) trace_mark(p, 4, it);
-      uint32_t sv[16], dpv[16];
-      tc::mbar_wait(&s_full[grp], (it >> 1) & 1);
-      if (warp == 4 || warp == 12) trace_mark(p, 5, it);
-      tc::tc_fence_after();
-      tmem_ld16(tmem + lane_base + C::T_S + 32 * grp + 16 * half, sv);
-      tc::mbar_wait(&dp_full[grp], (it >> 1) & 1);
-      if (warp == 4 || warp == 12) trace_mark(p, 6, it);
-      tc::tc_fence_after();
-      tmem_ld16(tmem + lane_base + C::T_DP + 32 * grp + 16 * half, dpv);
-      tc::tmem_ld_wait();
-      tc::tc_fence_before();
-      warp_arrive(&s_free[grp]);  // S^T_{it+2} may overwrite the score buffer
-      if (it >= 2) drain_dq(it - 2);  // dQ^T of this group's previous block (complete by now)
-      uint32_t wp[8], wd[8];
-      auto body = [&](auto masked) {
-#pragma unroll
-        for (int e = 0; e < 16; e += 4) {
-          const float4 l4 = lds_f4(nl + e), d4 = lds_f4(nd + e);  // warp broadcast
-          const bool poly = bwd_poly_group(2 * (e / 4));
-          float2 p0 = ex2x2_sel(poly, ffma2(u2f2(sv[e], sv[e + 1]), sc2, make_float2(l4.x, l4.y)));
-          float2 p1 = ex2x2_sel(poly, ffma2(u2f2(sv[e + 2], sv[e + 3]), sc2, make_float2(l4.z, l4.w)));
-          if constexpr (decltype(masked)::value) {
-            if (e < c_lo || e >= c_hi) p0.x = 0.f;
-            if (e + 1 < c_lo || e + 1 >= c_hi) p0.y = 0.f;
-            if (e + 2 < c_lo || e + 2 >= c_hi) p1.x = 0.f;
-            if (e + 3 < c_lo || e + 3 >= c_hi) p1.y = 0.f;
-          }
-          const float2 g0 = fmul2(p0, fadd2(u2f2(dpv[e], dpv[e + 1]), make_float2(d4.x, d4.y)));
-          const float2 g1 = fmul2(p1, fadd2(u2f2(dpv[e + 2], dpv[e + 3]), make_float2(d4.z, d4.w)));
-          wp[e / 2] = pack2(p0);
-          wp[e / 2 + 1] = pack2(p1);
-          wd[e / 2] = pack2(g0);
-          wd[e / 2 + 1] = pack2(g1);
-        }
-      };
-      if (prof_dbg(p) & 2) {
-        for (int e = 0; e < 8; ++e) wp[e] = wd[e] = sv[e] ^ dpv[e];
-      } else if (full_blk) {
-        body(std::false_type{});
-      } else {
-        body(std::true_type{});
-      }
-      // dS^T_it -> SMEM tile grp: row r (64 bytes), 16-byte chunks 2 half, 2 half + 1, 64-byte
-      // swizzle; once dQ^T_{it-2} finished reading the tile
-      if (it >= 2) tc::mbar_wait(&ds_free[grp], ((it >> 1) - 1) & 1);
-      {
-        uint8_t* row = sDS + grp * kDsBytes + r * 64;
-        const int sw = (r >> 1) & 3;
-        *reinterpret_cast<uint4*>(row + (((2 * half) ^ sw) << 4)) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-        *reinterpret_cast<uint4*>(row + (((2 * half + 1) ^ sw) << 4)) = make_uint4(wd[4], wd[5], wd[6], wd[7]);
-      }
-      tc::tmem_st8(tmem + lane_base + C::T_DP + 32 * grp + 16 * half, wp);      // P^T  -> [16 half, +8)
-      tc::tmem_st8(tmem + lane_base + C::T_DP + 32 * grp + 16 * half + 8, wd);  // dS^T -> [16 half + 8, +8)
-      tc::tmem_st_wait();
-      tc::fence_proxy_async_smem();  // dS^T visible to the dQ^T MMA (async proxy)
-      tc::tc_fence_before();
-      warp_arrive(&sm_done[grp]);
-      if (warp == 4 || warp == 12) trace_mark(p, 7, it);
-    }
-    // the last block of each group
-    {
-      const int last = niter - 1 - ((niter - 1 - grp) & 1);  // this group's last block (may be < 0)
-      if (last >= 0) drain_dq(last);
-    }
-    tc::mbar_wait(done, 0);
-    tc::tc_fence_after();
-    dkv_epilogue<HD>(p, sm, tmem, lane_base, C::T_DV, C::T_DK, r, g, warp, lane, j0, head);
-  }
-  tc::tc_fence_before();
-  tc::cluster_sync();  // no multicast data / remote arrive may target an exited CTA
-  tc::tc_fence_after();
-  if (warp == 1) tc::tmem_dealloc(tmem, 512);
-}
-
-// dQ accumulator -> bf16 dQ (times the softmax scale), 8 elements per thread.
-__global__ void dq_finish_k(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq, int64_t elems8, float scale) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < elems8;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float4 a = reinterpret_cast<const float4*>(acc)[2 * i], b = reinterpret_cast<const float4*>(acc)[2 * i + 1];
-    reinterpret_cast<uint4*>(dq)[i] = make_uint4(pack_bf16(a.x * scale, a.y * scale), pack_bf16(a.z * scale, a.w * scale),
-                                                 pack_bf16(b.x * scale, b.y * scale), pack_bf16(b.z * scale, b.w * scale));
-  }
 }
 
 // dQ: one CTA per (128-query block, head), looping over 64-key blocks:
@@ -1656,10 +1294,6 @@ void attn_fwd_tc(const void* q, const void* kv, void* o, float* lse, int64_t n, 
 }
 
 size_t attn_bwd_ws_delta_floats(int64_t n, int H) { return static_cast<size_t>(H) * ((n + 127) / 128 * 128) * 2; }
-// fused backward dQ accumulator [n_pad, H*hd] fp32 (the SIMT path uses the first n rows)
-size_t attn_bwd_ws_dq_floats(int64_t n, int H, int hd) {
-  return static_cast<size_t>((n + 127) / 128 * 128) * H * hd;
-}
 
 // Side stream of the calling thread's device for the dQ kernel: it runs concurrently
 // with the dK/dV kernel (both only read the prep output and write disjoint results),
@@ -1683,28 +1317,9 @@ SideStream& side_stream() {
 }
 }  // namespace
 
-#if SPK_ATTN_PROFILING
-// Profiling builds: cycle stamps of the traced CTA, relative to its first stamp.
-void print_trace(const unsigned long long* trace, cudaStream_t s, const char* which) {
-  unsigned long long h_t[16 * 64];
-  SPK_CUDA(cudaMemcpyAsync(h_t, trace, sizeof(h_t), cudaMemcpyDeviceToHost, s));
-  SPK_CUDA(cudaStreamSynchronize(s));
-  unsigned long long t0 = ~0ULL;
-  for (unsigned long long v : h_t)
-    if (v && v < t0) t0 = v;
-  std::fprintf(stderr, "%s trace (cycles from first stamp), events 0..15 per iteration\n", which);
-  for (int it = 0; it < 64; ++it) {
-    std::fprintf(stderr, "%3d", it);
-    for (int e = 0; e < 16; ++e)
-      std::fprintf(stderr, " %8lld", h_t[e * 64 + it] ? (long long)(h_t[e * 64 + it] - t0) : -1LL);
-    std::fprintf(stderr, "\n");
-  }
-}
-#endif
-
-void attn_bwd_tc(bool dkv_overwrite, bool split, const void* q, const void* kv, const void* o, const void* dout,
-                 const float* lse, float* ws_delta, float* ws_dq, void* dq, float* dkv, int64_t n, int64_t q_off,
-                 int64_t kv_len, int H, int hd, cudaStream_t s) {
+void attn_bwd_tc(bool dkv_overwrite, const void* q, const void* kv, const void* o, const void* dout, const float* lse, float* ws_delta,
+                 float* ws_dq, void* dq, float* dkv, int64_t n, int64_t q_off, int64_t kv_len, int H, int hd,
+                 cudaStream_t s) {
   const int h = H * hd;
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kv) | reinterpret_cast<uintptr_t>(dout) |
        reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(dq) | reinterpret_cast<uintptr_t>(dkv)) & 15)
@@ -1764,58 +1379,18 @@ void attn_bwd_tc(bool dkv_overwrite, bool split, const void* q, const void* kv, 
   a.dbg = 0;
   a.trace = nullptr;
 #if SPK_ATTN_PROFILING
-#ifndef SPK_ATTN_DBG_BITS
-#define SPK_ATTN_DBG_BITS 0
-#endif
-  a.dbg = SPK_ATTN_DBG_BITS;  // profiling builds only: skip MMAs / softmax (results invalid)
-  static unsigned long long* trace_buf = [] {  // profiling builds trace every backward call
+  a.dbg = [] {
+    const char* e = std::getenv("SP_ATTN_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  static unsigned long long* trace_buf = [] {
     unsigned long long* t = nullptr;
-    SPK_CUDA(cudaMalloc(&t, 16 * 64 * sizeof(unsigned long long)));
+    if (std::getenv("SP_ATTN_TRACE")) SPK_CUDA(cudaMalloc(&t, 16 * 64 * sizeof(unsigned long long)));
     return t;
   }();
   a.trace = trace_buf;
   if (trace_buf) SPK_CUDA(cudaMemsetAsync(trace_buf, 0, 16 * 64 * sizeof(unsigned long long), s));
 #endif
-  a.dq_acc = ws_dq;
-  if (!split && hd <= 80) {
-    // Fused kernel: dK/dV and dQ from one pass (no S / dP recompute); dQ accumulates in
-    // fp32 and is scaled into bf16 afterwards.
-    SPK_CUDA(cudaMemsetAsync(ws_dq, 0, sizeof(float) * attn_bwd_ws_dq_floats(n, H, hd), s));
-    AttnBwdParams f = a;  // Q / dO in 32-row tiles
-    make_maps(&f.tq, q, h, n, hd, FBQ);
-    make_maps(&f.tdo, dout, h, n, hd, FBQ);
-    auto runf = [&](auto hd_tag) {
-      constexpr int HD = decltype(hd_tag)::value;
-      constexpr size_t smem = fused_smem<HD>();
-      static_assert(smem <= 232448, "fused attention bwd smem");
-      SPK_CUDA(cudaFuncSetAttribute(attn_bwd_fused_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3(static_cast<unsigned>(((kv_len + 127) / 128 + 1) & ~int64_t(1)), static_cast<unsigned>(H));
-      lc.blockDim = dim3(640);
-      lc.dynamicSmemBytes = smem;
-      lc.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = 2;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      lc.attrs = at;
-      lc.numAttrs = 1;
-      SPK_CUDA(cudaLaunchKernelEx(&lc, attn_bwd_fused_k<HD>, f));
-#if SPK_ATTN_PROFILING
-      print_trace(a.trace, s, "fused");
-#endif
-    };
-    if (hd == 64)
-      runf(std::integral_constant<int, 64>{});
-    else
-      runf(std::integral_constant<int, 80>{});
-    const int64_t e8 = n * h / 8;
-    dq_finish_k<<<static_cast<unsigned>(std::min<int64_t>((e8 + 255) / 256, 148 * 8)), 256, 0, s>>>(
-        ws_dq, static_cast<__nv_bfloat16*>(dq), e8, a.scale);
-    SPK_LAUNCH_CHECK();
-    return;
-  }
   AttnBwdParams b = a;  // dQ kernel: K/V in 64-row tiles (Q / dO go to TMEM from the raw rows)
   b.trace = nullptr;
   make_maps(&b.tkv, kv, 2 * h, kv_len, hd, 64);
@@ -1857,7 +1432,22 @@ void attn_bwd_tc(bool dkv_overwrite, bool split, const void* q, const void* kv, 
       }
       SPK_CUDA(cudaLaunchKernelEx(&lc, attn_bwd_dkv_k<HD>, a));
 #if SPK_ATTN_PROFILING
-      if (a.trace) print_trace(a.trace, s, "dkv");
+      if (a.trace) {
+        unsigned long long h_t[16 * 64];
+        SPK_CUDA(cudaMemcpyAsync(h_t, a.trace, sizeof(h_t), cudaMemcpyDeviceToHost, s));
+        SPK_CUDA(cudaStreamSynchronize(s));
+        unsigned long long t0 = ~0ULL;
+        for (unsigned long long v : h_t)
+          if (v && v < t0) t0 = v;
+        std::fprintf(stderr, "dkv trace (cycles from first stamp): it q_load g_issue dp_issue s_issue sm_qfull sm_s sm_dp sm_done\n");
+        std::fprintf(stderr, "epilogue start %lld end %lld\n", (long long)(h_t[8 * 64] - t0), (long long)(h_t[9 * 64] - t0));
+        for (int it = 0; it < 64; ++it) {
+          std::fprintf(stderr, "%3d", it);
+          for (int e = 0; e < 8; ++e)
+            std::fprintf(stderr, " %8lld", h_t[e * 64 + it] ? (long long)(h_t[e * 64 + it] - t0) : -1LL);
+          std::fprintf(stderr, "\n");
+        }
+      }
 #endif
     }
     dim3 g2(static_cast<unsigned>((n + 127) / 128), static_cast<unsigned>(H));

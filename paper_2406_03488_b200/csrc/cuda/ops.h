@@ -52,17 +52,14 @@ void gemm_tcgen05(const GemmArgs& a, cudaStream_t s);
 // q [n, H*hd] (row stride H*hd), kv [kv_len, 2*H*hd] (K | V per row),
 // o [n, H*hd], lse [H, n] fp32. Query i has global position q_off + i and may
 // attend to keys j <= q_off + i (j < kv_len).
-// kAttnTensorSplit: bf16 backward through the separate dK/dV and dQ (recompute) kernels
-// -- the head-dim-128 path, selectable at hd <= 80 for comparison with the fused kernel.
-enum AttnImpl : int { kAttnAuto = 0, kAttnSimt = 1, kAttnTensor = 2, kAttnTensorSplit = 3 };
+enum AttnImpl : int { kAttnAuto = 0, kAttnSimt = 1, kAttnTensor = 2 };
 void attn_fwd(DType t, int impl, const void* q, const void* kv, void* o, float* lse, int64_t n, int64_t q_off,
               int64_t kv_len, int H, int hd, cudaStream_t s);
 // dq [n, H*hd] (dtype t); dkv_acc [kv_len, 2*H*hd] fp32, accumulated (+=), or written
 // (=) when dkv_overwrite (every row [0, kv_len) is covered by the call: the first
 // backward op of a micro-batch, which saves the accumulator's memset and read).
-// ws_delta: >= attn_bwd_ws_delta_floats(n, H) floats; ws_dq: >= attn_bwd_ws_dq_floats(n, H, hd) floats.
+// ws_delta: >= attn_bwd_ws_delta_floats(n, H) floats; ws_dq: >= n*H*hd floats.
 size_t attn_bwd_ws_delta_floats(int64_t n, int H);
-size_t attn_bwd_ws_dq_floats(int64_t n, int H, int hd);
 void attn_bwd(DType t, int impl, const void* q, const void* kv, const void* o, const void* dout, const float* lse,
               float* ws_delta, float* ws_dq, void* dq, float* dkv_acc, int64_t n, int64_t q_off, int64_t kv_len, int H,
               int hd, cudaStream_t s, bool dkv_overwrite = false);

@@ -161,7 +161,7 @@ Stage::Stage(const ModelCfg& m, const seqpipe::ScenarioConfig& cfg, const std::v
   SPK_CUDA(cudaMalloc(&w_t3_, esz_ * n * h));
   SPK_CUDA(cudaMalloc(&w_dqkv_, esz_ * n * 3 * h));
   SPK_CUDA(cudaMalloc(&w_delta_, sizeof(float) * spk::attn_bwd_ws_delta_floats(n, mc_.H)));
-  SPK_CUDA(cudaMalloc(&w_dq_, sizeof(float) * spk::attn_bwd_ws_dq_floats(n, mc_.H, mc_.hd)));
+  SPK_CUDA(cudaMalloc(&w_dq_, sizeof(float) * n * h));
   if (last()) {
     SPK_CUDA(cudaMalloc(&w_fmean_, sizeof(float) * n));
     SPK_CUDA(cudaMalloc(&w_frstd_, sizeof(float) * n));

@@ -1,8 +1,7 @@
 #!/usr/bin/env python
 """SM clock / power / throttle reasons while the attention kernels run back to back:
-attn_clock.py [fwd|bwd|bwd-split] [n q_off H hd]. Prints ms per call, algorithmic TFLOP/s
-(fwd 4*H*hd*(n*q_off + n^2/2), bwd twice that) and the median SM clock. bwd = the default
-backward (fused at hd <= 80), bwd-split = the split dK/dV + dQ-recompute kernels (impl 3)."""
+attn_clock.py [fwd|bwd] [n q_off H hd]. Prints ms per call, algorithmic TFLOP/s
+(fwd 4*H*hd*(n*q_off + n^2/2), bwd twice that) and the median SM clock."""
 import ctypes as C
 import sys
 import threading
@@ -32,7 +31,7 @@ def fwd():
     _capi.check(lib.sp_attention_fwd(1, 0, P(q), P(kv), P(o), P(lse), n, q_off, L, H, hd, C.c_void_p(s)))
 
 
-BWD_IMPL = 3 if which == "bwd-split" else 0
+BWD_IMPL = 0
 
 
 def bwd():
