@@ -262,6 +262,50 @@ def run_reference(args, rank, world):
     return 0
 
 
+def stage1_budget(W, preset, args, E, pl):
+    """Stage 1 of the workload's full pipeline (P = W["pipeline"], M = 2P): does it fit one B200?
+    HBM of the stage = weights + grads + AdamW m/v (fp32) + bf16 compute copy (18 B/param; stage 1
+    also holds the token / position embeddings) + the fp32 dK/dV accumulator + the activation arena
+    (engine plan, offline-placed; sp_plan_memory) + per-op workspaces. If it does not fit, the plan
+    that does: recompute the MLP up-projection output u in B instead of storing it (u is the largest
+    per-token field of a record), priced in extra FLOPs."""
+    import torch
+    P = W["pipeline"]
+    M = 2 * P
+    h, F, L, V = W["h"], W["F"], W["L"], W["V"]
+    c = pl.preset_scenario(preset)
+    for key, v in (("pipeline_size", P), ("seq_len", args.seq), ("segments", args.k), ("micro_batches", M)):
+        pl.apply_scenario_override(c, key, str(v))
+    part = pl.partition_for(c, args.partition)
+
+    def model(ffn):
+        return E.ModelConfig(family=W["family"], dtype=E.BF16, vocab=V, hidden=h, layers=L, heads=W["H"],
+                             head_dim=W["hd"], ffn=ffn, max_seq=args.seq)
+    live, arena, dkv = E.plan_memory(c, "seq1f1b", part, model(F), stage=1)
+    live_nou, arena_nou, _ = E.plan_memory(c, "seq1f1b", part, model(64), stage=1)
+    fup = 2 * F if W["family"] == LLAMA else F
+    per_layer = 4 * h * h + (3 if W["family"] == LLAMA else 2) * h * F + 4 * h
+    params = (L // P) * per_layer + V * h + (args.seq * h if W["family"] == GPT else 0)
+    weights = 18 * params
+    n = max(part.lengths)
+    ws = 2 * n * (h + 2 * fup + 6 * h) + 4 * n * h + 8 * n * W["H"]
+    cap = torch.cuda.mem_get_info(0)[1] if torch.cuda.is_available() else 180e9
+    total = weights + dkv + arena + ws
+    total_rc = weights + dkv + arena_nou + ws
+    n_tok = sum(part.lengths)
+    layer_fl = 2 * n_tok * per_layer  # forward GEMM FLOPs of a layer over the sequence (approx.)
+    extra = 2 * n_tok * h * fup / (3 * layer_fl)
+    gb = 1e9
+    return {"pipeline": P, "micro_batches": M, "segments": args.k, "partition": args.partition,
+            "weights_optimizer_gb": weights / gb, "dkv_accumulator_gb": dkv / gb, "arena_gb": arena / gb,
+            "live_activation_peak_gb": live / gb, "workspaces_gb": ws / gb, "total_gb": total / gb,
+            "device_capacity_gb": cap / gb, "fits": total <= cap,
+            "if_oom_plan": None if total <= cap else {
+                "recompute": "MLP up-projection output u recomputed in B (one extra [n,h]x[h,Fup] GEMM per layer)",
+                "arena_gb": arena_nou / gb, "live_activation_peak_gb": live_nou / gb, "total_gb": total_rc / gb,
+                "fits": total_rc <= cap, "extra_gemm_flops_frac": extra}}
+
+
 def config_of(args, micro, seq, k, lengths):
     W = WORKLOADS[args.workload]
     return {"workload": W["desc"], "model": W["model"], "global_batch": micro, "seq_len": seq, "segments": k,
@@ -439,6 +483,8 @@ def main():
         except Exception as e:  # pragma: no cover
             memory_model[f"P{P}"] = {"error": str(e)}
 
+    stage1 = stage1_budget(W, preset, args, E, pl) if W["stage_layers"] else None
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -472,6 +518,7 @@ def main():
             "device_memory_gb": {"engine_allocated": mem[0] / 1e9, "device_free": mem[1] / 1e9,
                                  "activation_arena": last.arena_bytes / 1e9},
             "memory_model": memory_model,
+            **({"stage1_budget_full_pipeline": stage1} if stage1 else {}),
             "roofline": {"bound": "tensor", "kernel": names[dom], "achieved": achieved, "peak": sustained,
                          "peak_kind": f"bf16 sustained ({src})", "peak_burst": burst, "unit": "TFLOP/s",
                          "frac": (achieved / sustained) if achieved else None,
