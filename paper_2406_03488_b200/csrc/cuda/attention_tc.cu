@@ -133,6 +133,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 
+__device__ __forceinline__ int clamp_i32(int64_t v) {  // to +-2^30: mask bounds stay exact
+  return static_cast<int>(v < -(int64_t(1) << 30) ? -(int64_t(1) << 30) : (v > (int64_t(1) << 30) ? (int64_t(1) << 30) : v));
+}
+
 // One MUFU.EX2 (exp2f() adds range-reduction FMUL/FSETP/FSEL around it).
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -858,25 +862,37 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
       warp_arrive(kv_full);
     }
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-    for (int it = 0; it < niter; ++it) {
-      const int b = it % NS, st = it % QST, d = it % ND;
-      const int64_t i0 = ib0 + static_cast<int64_t>(it) * 64;
+    // Per-iteration bookkeeping as running counters: ring / buffer indices and mbarrier
+    // parities advance without div / mod, and the causal-mask bounds are int32 values
+    // stepped by 64 (the 64-bit per-iteration index math was ~2 instructions per score).
+    // Visible query columns c (local) of block it: c >= cmin, c < chi, where
+    // cmin = kpos - q_off - (ib0 + 64 it + 16g) and chi = n - (ib0 + 64 it + 16g).
+    int b = 0, st = 0, d = 0;
+    uint32_t ph_b = 0, ph_st = 0, ph_d = 0;
+    int cmin = clamp_i32(kpos - p.q_off - ib0 - g * 16);
+    int cmin_w = clamp_i32(j0 + quarter * 32 + 31 - p.q_off - ib0 - g * 16);  // the warp's largest cmin
+    int chi = clamp_i32(p.n - ib0 - g * 16);
+    auto advance = [&] {
+      cmin -= 64;
+      cmin_w -= 64;
+      chi -= 64;
+      if (++b == NS) b = 0, ph_b ^= 1;
+      if (++st == QST) st = 0, ph_st ^= 1;
+      if (++d == ND) d = 0, ph_d ^= 1;
+    };
+    for (int it = 0; it < niter; ++it, advance()) {
       const float* nl = sLD + st * 128 + g * 16;  // -LSE*log2e of this group's 16 queries
       const float* nd = nl + 64;                  // -delta of the same queries
-      // visible query columns c (local): q_off + i0 + 16g + c >= kpos, i0 + 16g + c < n
-      const int64_t cbase = i0 + g * 16;
-      const int64_t cmin = kpos - p.q_off - cbase;
-      const int c_lo = cmin < 0 ? 0 : (cmin > 16 ? 16 : static_cast<int>(cmin));
-      const int64_t chi = p.n - cbase;
-      const int c_hi = chi < 0 ? 0 : (chi > 16 ? 16 : static_cast<int>(chi));  // exclusive
-      const bool full_blk = __all_sync(0xffffffffu, c_lo == 0 && c_hi == 16);
-      tc::mbar_wait(&q_full[st], (it / QST) & 1);  // LSE / delta of this block are in SMEM
+      const int c_lo = cmin < 0 ? 0 : (cmin > 16 ? 16 : cmin);
+      const int c_hi = chi < 0 ? 0 : (chi > 16 ? 16 : chi);  // exclusive
+      const bool full_blk = cmin_w <= 0 && chi >= 16;        // warp-uniform
+      tc::mbar_wait(&q_full[st], ph_st);  // LSE / delta of this block are in SMEM
       if (warp == 4) trace_mark(p, 4, it);
       uint32_t sv[16], dpv[16];
-      tc::mbar_wait(&s_full[b], (it / NS) & 1);
+      tc::mbar_wait(&s_full[b], ph_b);
       if (warp == 4) trace_mark(p, 5, it);
       if (prof_dbg(p) & 2) {  // protocol only
-        tc::mbar_wait(&dp_full[d], (it / ND) & 1);
+        tc::mbar_wait(&dp_full[d], ph_d);
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&dp_free[d]);
         warp_arrive(&sm_done[b]);
@@ -884,7 +900,7 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
       }
       tc::tc_fence_after();
       tmem_ld16(tmem + lane_base + b * 64 + g * 16, sv);
-      tc::mbar_wait(&dp_full[d], (it / ND) & 1);
+      tc::mbar_wait(&dp_full[d], ph_d);
       if (warp == 4) trace_mark(p, 6, it);
       tc::tc_fence_after();
       tmem_ld16(tmem + lane_base + C::T_DP + d * 64 + g * 16, dpv);
@@ -1135,17 +1151,22 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dq_k(const __grid_constant__ 
     const int64_t ldi = (static_cast<int64_t>(head) * p.n_pad + (row & ~int64_t(63))) * 2 + (row & 63);
     const float2 nl2 = make_float2(p.ld[ldi], p.ld[ldi]), nd2 = make_float2(p.ld[ldi + 64], p.ld[ldi + 64]);
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-    for (int j = 0; j < nblk; ++j) {
-      const int b = j % NS, d = j % ND;
-      // key columns c (local) with j*64 + 16g + c <= qpos are visible
-      const int64_t lim64 = valid ? qpos - static_cast<int64_t>(j) * 64 - g * 16 : -1;
-      const int lim = lim64 > 1000 ? 1000 : static_cast<int>(lim64);
-      const bool full_blk = __all_sync(0xffffffffu, lim >= 15);
+    // running counters as in the dK/dV kernel: key columns c (local) with c <= lim are
+    // visible, lim = qpos - 64 j - 16g (-1 for rows past n); the warp's smallest lim is
+    // that of its first row.
+    int b = 0, d = 0;
+    uint32_t ph_b = 0, ph_d = 0;
+    int lim_r = valid ? clamp_i32(qpos - g * 16) : -(1 << 30);
+    const bool warp_valid = q0 + quarter * 32 + 31 < p.n;
+    int lim_w = clamp_i32(p.q_off + q0 + quarter * 32 - g * 16);
+    for (int j = 0; j < nblk; ++j, lim_r -= 64, lim_w -= 64) {
+      const int lim = lim_r < -1 ? -1 : (lim_r > 1000 ? 1000 : lim_r);
+      const bool full_blk = warp_valid && lim_w >= 15;  // warp-uniform
       uint32_t sv[16], dpv[16];
-      tc::mbar_wait(&s_full[b], (j / NS) & 1);
+      tc::mbar_wait(&s_full[b], ph_b);
       tc::tc_fence_after();
       tmem_ld16(tmem + lane_base + b * 64 + g * 16, sv);
-      tc::mbar_wait(&dp_full[d], (j / ND) & 1);
+      tc::mbar_wait(&dp_full[d], ph_d);
       tc::tc_fence_after();
       tmem_ld16(tmem + lane_base + C::T_DP + d * 64 + g * 16, dpv);
       tc::tmem_ld_wait();
@@ -1172,6 +1193,8 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dq_k(const __grid_constant__ 
       tc::tmem_st_wait();
       tc::tc_fence_before();
       warp_arrive(&ds_full[b]);
+      if (++b == NS) b = 0, ph_b ^= 1;
+      if (++d == ND) d = 0, ph_d ^= 1;
     }
     tc::mbar_wait(done, 0);
     tc::tc_fence_after();

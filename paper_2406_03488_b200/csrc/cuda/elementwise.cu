@@ -374,8 +374,74 @@ __global__ void __launch_bounds__(256) norm_fwd_vec_k(const __nv_bfloat16* __res
   }
 }
 
+// Rows of h >= 2048 (NV even): two warps per row, each caching half of it (NV/2 16-byte
+// vectors per lane, ~20 registers), so 4 CTAs = 32 warps fit per SM and every load of a
+// row is in flight at once. Each half computes its own mean and centred sum of squares
+// (two passes over registers) and the pair combines them through shared memory in one
+// exchange (Chan: M2 = M2_a + M2_b + (mean_a - mean_b)^2 * H/4), which keeps the
+// two-pass numerics. The one-warp-per-row kernel above held the whole row (128 registers,
+// 16 warps per SM) and reached 0.53 of HBM.
 template <int NV, bool RMS>
-__global__ void __launch_bounds__(256) norm_apply_vec_k(const __nv_bfloat16* __restrict__ x, const float* __restrict__ g,
+__global__ void __launch_bounds__(256, NV <= 12 ? 4 : (NV <= 16 ? 3 : 2)) norm_fwd_pair_k(const __nv_bfloat16* __restrict__ x,
+                                                          const float* __restrict__ g, __nv_bfloat16* __restrict__ y,
+                                                          float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                          int64_t n, float eps) {
+  constexpr int H = 256 * NV, NH = NV / 2;
+  __shared__ float2 xch[4][2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, pr = w >> 1, hw = w & 1;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 4 + pr;
+  const bool ok = row < n;
+  const Bf8* xr = reinterpret_cast<const Bf8*>(x + (ok ? row : 0) * H) + hw * NH * 32;
+  Bf8 xv[NH];
+#pragma unroll
+  for (int k = 0; k < NH; ++k) xv[k] = xr[k * 32 + lane];
+  float s = 0.f;
+  if (!RMS) {
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      float f[8];
+      bf8_to_f(xv[k], f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += f[e];
+    }
+    s = warp_sum(s);
+  }
+  const float mh = RMS ? 0.f : s * (2.f / H);  // this half's mean
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < NH; ++k) {
+    float f[8];
+    bf8_to_f(xv[k], f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ss += (f[e] - mh) * (f[e] - mh);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) xch[pr][hw] = make_float2(mh, ss);
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + pr) : "memory");
+  const float2 o = xch[pr][hw ^ 1];
+  const float mean = RMS ? 0.f : 0.5f * (mh + o.x);
+  const float d = mh - o.x;
+  const float rstd = rsqrtf((ss + o.y + (RMS ? 0.f : d * d * (H / 4))) / H + eps);
+  if (!ok) return;
+  Bf8* yr = reinterpret_cast<Bf8*>(y + row * H) + hw * NH * 32;
+  const float* gh = g + hw * (H / 2);
+#pragma unroll
+  for (int k = 0; k < NH; ++k) {
+    float f[8], gv[8];
+    bf8_to_f(xv[k], f);
+    ld_f8(gh + (k * 32 + lane) * 8, gv);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = (f[e] - mean) * rstd * gv[e];
+    yr[k * 32 + lane] = f_to_bf8(f);
+  }
+  if (lane == 0 && hw == 0) {
+    if (!RMS) mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+template <int NV, bool RMS>
+__global__ void __launch_bounds__(256, 4) norm_apply_vec_k(const __nv_bfloat16* __restrict__ x, const float* __restrict__ g,
                                                         const float* __restrict__ mean, const float* __restrict__ rstd,
                                                         __nv_bfloat16* __restrict__ y, int64_t n) {
   constexpr int H = 256 * NV;
@@ -385,10 +451,15 @@ __global__ void __launch_bounds__(256) norm_apply_vec_k(const __nv_bfloat16* __r
   const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
   const Bf8* xr = reinterpret_cast<const Bf8*>(x + row * H);
   Bf8* yr = reinterpret_cast<Bf8*>(y + row * H);
+  // every 16-byte load of the row in flight at once (one DRAM round trip per row; issued
+  // per chunk inside the output loop they were ten dependent round trips)
+  Bf8 xv[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) xv[k] = xr[k * 32 + lane];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     float f[8], gv[8];
-    bf8_to_f(xr[k * 32 + lane], f);
+    bf8_to_f(xv[k], f);
     ld_f8(g + (k * 32 + lane) * 8, gv);
 #pragma unroll
     for (int e = 0; e < 8; ++e) f[e] = (f[e] - mu) * rs * gv[e];
@@ -501,11 +572,15 @@ __global__ void __launch_bounds__(256, 2) norm_bwd_pair_k(const __nv_bfloat16* _
     const Bf8* dyr = reinterpret_cast<const Bf8*>(dy + row * H) + hw * NH * 32;
     const float* gh = g + hw * HH;
     const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
-    Bf8 xv[NH], dv[NH];
+    const Bf8* drr = dres ? reinterpret_cast<const Bf8*>(dres + row * H) + hw * NH * 32 : nullptr;
+    // the residual gradient is loaded with x and dy (one DRAM round trip per row; loaded in
+    // the output pass it was a second, dependent one)
+    Bf8 xv[NH], dv[NH], rv[NH];
 #pragma unroll
     for (int k = 0; k < NH; ++k) {
       xv[k] = xr[k * 32 + lane];
       dv[k] = dyr[k * 32 + lane];
+      if (drr) rv[k] = drr[k * 32 + lane];
     }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -538,14 +613,13 @@ __global__ void __launch_bounds__(256, 2) norm_bwd_pair_k(const __nv_bfloat16* _
     const float m1 = RMS ? 0.f : (s1 + slot[(hw ^ 1) * 2]) / H;
     const float m2 = (s2 + slot[(hw ^ 1) * 2 + 1]) / H;
     Bf8* dxr = reinterpret_cast<Bf8*>(dx + row * H) + hw * NH * 32;
-    const Bf8* drr = dres ? reinterpret_cast<const Bf8*>(dres + row * H) + hw * NH * 32 : nullptr;
 #pragma unroll
     for (int k = 0; k < NH; ++k) {
       float f[8], d[8], gv[8], r[8];
       bf8_to_f(xv[k], f);
       bf8_to_f(dv[k], d);
       ld_f8(gh + (k * 32 + lane) * 8, gv);
-      if (drr) bf8_to_f(drr[k * 32 + lane], r);
+      if (drr) bf8_to_f(rv[k], r);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const float xh = (f[e] - mu) * rs;
@@ -750,9 +824,17 @@ void norm_fwd(DType t, bool rms, const void* x, const float* g, void* y, float* 
   if (n == 0) return;
   if (t == DType::kBF16 && dispatch_nv(h, [&](auto nv) {
         constexpr int NV = decltype(nv)::value;
-        const unsigned grid = static_cast<unsigned>((n + 7) / 8);
         const auto* xb = static_cast<const __nv_bfloat16*>(x);
         auto* yb = static_cast<__nv_bfloat16*>(y);
+        if constexpr (NV >= 8 && NV % 2 == 0) {
+          const unsigned grid = static_cast<unsigned>((n + 3) / 4);
+          if (rms)
+            norm_fwd_pair_k<NV, true><<<grid, 256, 0, s>>>(xb, g, yb, mean, rstd, n, eps);
+          else
+            norm_fwd_pair_k<NV, false><<<grid, 256, 0, s>>>(xb, g, yb, mean, rstd, n, eps);
+          return;
+        }
+        const unsigned grid = static_cast<unsigned>((n + 7) / 8);
         if (rms)
           norm_fwd_vec_k<NV, true><<<grid, 256, 0, s>>>(xb, g, yb, mean, rstd, n, eps);
         else

@@ -199,6 +199,13 @@ void Engine::comm_init(const std::vector<std::string>& ids) {
 void Engine::attach_local(std::shared_ptr<LocalHub> hub) {
   if (world_ == 1) return;
   SPK_CUDA(cudaSetDevice(dev_));
+  size_t sends = 0, max_bytes = 0;
+  for (const sp_comm_op& c : plan_)
+    if (c.dir == SP_COMM_SEND) {
+      ++sends;
+      max_bytes = std::max(max_bytes, spk::dtype_size(mc_.dt) * static_cast<size_t>(c.elems));
+    }
+  if (sends) local_hub_reserve(hub, dev_, sends, max_bytes);
   transport_ = make_local_transport(std::move(hub), rank_);
   comm_ready_setup();
 }

@@ -111,6 +111,21 @@ struct LocalHub {
       if (s.freed) cudaEventDestroy(s.freed);
     }
   }
+  // Staging slots allocated before any step: a cudaMalloc inside a step (while another rank's
+  // host thread is blocked on this hub and its streams wait on events it has yet to enqueue)
+  // could serialise against the device and stall every rank.
+  void reserve(int dev, size_t n, size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (size_t i = 0; i < n; ++i) {
+      Slot s;
+      s.cap = bytes;
+      s.device = dev;
+      SPK_CUDA(cudaMalloc(&s.ptr, bytes));
+      SPK_CUDA(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
+      SPK_CUDA(cudaEventCreateWithFlags(&s.freed, cudaEventDisableTiming));
+      slots.push_back(s);
+    }
+  }
   // A staging buffer of >= bytes on the calling thread's device (caller holds mu).
   size_t acquire(size_t bytes) {
     int dev = 0;
@@ -220,6 +235,10 @@ class LocalTransport final : public Transport {
 
 std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalHub> hub, int rank) {
   return std::make_unique<LocalTransport>(std::move(hub), rank);
+}
+
+void local_hub_reserve(const std::shared_ptr<LocalHub>& hub, int device, size_t slots, size_t bytes) {
+  hub->reserve(device, slots, bytes);
 }
 
 }  // namespace spe

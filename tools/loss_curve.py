@@ -32,6 +32,8 @@ for graph in (False, True):
         losses.append(eng.step(tok).loss)
         if i == 0 and graph:
             eng.enable_graph(True)
+    # loss of an unseen batch before its update: memorisation does not carry over, a leak would
+    held = eng.step(np.random.default_rng(99).integers(0, W["V"], size=(2, W["seq"] + 1)).astype(np.int32)).loss
     print(f"{w} layers {layers} graph {graph}: ln V = {np.log(W['V']):.3f}, losses " +
-          " ".join(f"{x:.4f}" for x in losses), flush=True)
+          " ".join(f"{x:.4f}" for x in losses) + f", held-out batch {held:.4f}", flush=True)
     eng.close()

@@ -15,9 +15,12 @@ Per stage it reports what the device holds, measured:
                          structure's idle under sharing, not the P-GPU bubble (BASELINE.md §3
                          carries the modeled one, printed next to it).
 
-python tools/pipeline_inproc.py [--P 4] [--layers-per-stage 2] [--seq 32768] [--micro 8] [--k 4]
-Prints one JSON line per schedule kind."""
+python tools/pipeline_inproc.py [--model gpt-2.7b|llama-7b] [--P 4] [--layers-per-stage 2] [--seq 32768]
+                                [--micro 8] [--k 4] [--sweep T:k:P,...]
+Prints one JSON line per (schedule kind, point). --sweep runs the cfg-5 grid points given (k = 1 is
+batch-level 1F1B, reference test_schedules.cpp:163-170) with M = 2P."""
 import argparse
+import faulthandler
 import json
 import sys
 import threading
@@ -29,16 +32,17 @@ import torch  # noqa: E402
 from paper_2406_03488_b200 import engine as E  # noqa: E402
 from paper_2406_03488_b200 import planner as pl  # noqa: E402
 
-GPT = E.GPT
+MODELS = {"gpt-2.7b": dict(family=E.GPT, vocab=50257, hidden=2560, heads=32, head_dim=80, ffn=10240),
+          "llama-7b": dict(family=E.LLAMA, vocab=32000, hidden=4096, heads=32, head_dim=128, ffn=11008)}
 
 
-def run(kind, P, lps, seq, micro, k, mode):
+def run(kind, P, lps, seq, micro, k, mode, model_name="gpt-2.7b"):
     layers = P * lps
-    model = E.ModelConfig(family=GPT, dtype=E.BF16, vocab=50257, hidden=2560, layers=layers, heads=32, head_dim=80,
-                          ffn=10240, max_seq=seq, seed=42)
+    mk = MODELS[model_name]
+    model = E.ModelConfig(dtype=E.BF16, layers=layers, max_seq=seq, seed=42, **mk)
     segs = k if kind.startswith("seq") else 1
     cfg = pl.ScenarioConfig(pipeline_size=P, micro_batches=micro, segments=segs, seq_len=seq, layers=layers,
-                            hidden_dim=2560, param_count=model.param_count())
+                            hidden_dim=mk["hidden"], param_count=model.param_count())
     cfg.validate()
     part = pl.partition_for(cfg, mode if segs > 1 else "even")
     hub = E.LocalHub(P, watchdog_seconds=600.0)
@@ -54,6 +58,7 @@ def run(kind, P, lps, seq, micro, k, mode):
         dev_bytes.append(free0 - free1)
     tok = torch.randint(0, model.vocab, (micro, seq + 1), dtype=torch.int32).numpy()
     out = {}
+    print(f"# {kind} P={P} engines built", file=sys.stderr, flush=True)
     for it in range(2):  # step 0 warms up (graph-free path, lazy workspaces), step 1 is reported
         reps, errs = [None] * P, [None] * P
 
@@ -70,6 +75,7 @@ def run(kind, P, lps, seq, micro, k, mode):
             t.join()
         if any(errs):
             raise RuntimeError(errs)
+        print(f"# {kind} step {it} done", file=sys.stderr, flush=True)
         out = reps
     stages = []
     for r, rep in enumerate(out):
@@ -87,7 +93,8 @@ def run(kind, P, lps, seq, micro, k, mode):
         e.close()
     del hub
     torch.cuda.empty_cache()
-    return {"kind": kind, "P": P, "layers_per_stage": lps, "seq": seq, "micro_batches": micro, "segments": segs,
+    return {"model": model_name, "kind": kind, "P": P, "layers_per_stage": lps, "seq": seq, "micro_batches": micro,
+            "segments": segs,
             "partition": list(part.lengths), "stages": stages,
             "modeled_bubble_ratio": float(modeled.aggregate_bubble_ratio),
             "loss": out[-1].loss}
@@ -102,10 +109,21 @@ def main():
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--partition", default="cwp")
     ap.add_argument("--kinds", default="seq1f1b,1f1b")
+    ap.add_argument("--model", default="gpt-2.7b", choices=sorted(MODELS))
+    ap.add_argument("--sweep", default="")
+    ap.add_argument("--dump-after", type=float, default=600.0, help="dump every thread's stack after this many s")
     a = ap.parse_args()
+    faulthandler.dump_traceback_later(a.dump_after, exit=False)
+    if a.sweep:
+        for pt in a.sweep.split(","):
+            T, k, P = (int(v) for v in pt.split(":"))
+            kind = "seq1f1b" if k > 1 else "1f1b"
+            r = run(kind, P, a.layers_per_stage, T, 2 * P, k, a.partition, a.model)
+            print(json.dumps(r), flush=True)
+        return
     res = {}
     for kind in a.kinds.split(","):
-        res[kind] = run(kind, a.P, a.layers_per_stage, a.seq, a.micro, a.k, a.partition)
+        res[kind] = run(kind, a.P, a.layers_per_stage, a.seq, a.micro, a.k, a.partition, a.model)
         print(json.dumps(res[kind]), flush=True)
     if "seq1f1b" in res and "1f1b" in res:
         s, b = res["seq1f1b"]["stages"][0], res["1f1b"]["stages"][0]
