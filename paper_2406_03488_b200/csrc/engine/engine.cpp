@@ -205,8 +205,7 @@ void Engine::attach_local(std::shared_ptr<LocalHub> hub) {
       ++sends;
       max_bytes = std::max(max_bytes, spk::dtype_size(mc_.dt) * static_cast<size_t>(c.elems));
     }
-  if (sends) local_hub_reserve(hub, dev_, sends, max_bytes);
-  transport_ = make_local_transport(std::move(hub), rank_);
+  transport_ = make_local_transport(std::move(hub), rank_, sends, max_bytes);
   comm_ready_setup();
 }
 

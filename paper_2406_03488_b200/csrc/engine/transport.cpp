@@ -88,6 +88,7 @@ struct LocalHub {
     cudaEvent_t ready = nullptr;  // recorded on the sender stream after the copy in
     cudaEvent_t freed = nullptr;  // recorded on the receiver stream after the copy out
     bool busy = false, used = false;
+    int owner = -1;  // rank that reserved it (its sends only, in a fixed rotation), -1 = shared pool
   };
   struct Msg {
     size_t slot;
@@ -111,20 +112,29 @@ struct LocalHub {
       if (s.freed) cudaEventDestroy(s.freed);
     }
   }
-  // Staging slots allocated before any step: a cudaMalloc inside a step (while another rank's
-  // host thread is blocked on this hub and its streams wait on events it has yet to enqueue)
-  // could serialise against the device and stall every rank.
-  void reserve(int dev, size_t n, size_t bytes) {
+  // Staging slots owned by one rank, allocated before any step, one per send of its step: the
+  // i-th send of a step always uses slot i. A slot shared by all ranks and reused as soon as
+  // its receiver had *enqueued* the copy-out made the next sender's stream wait (on the GPU)
+  // for that copy-out, which waits for the receiver's compute, which can wait for the next
+  // sender -- a cross-rank cycle that hung a 4-stage GPT-2.7B step on one GPU. With owned
+  // slots a slot is reused only by the same send of the next step, whose copy-out depends on
+  // the previous step alone. (It also keeps cudaMalloc out of the step.)
+  std::vector<size_t> reserve(int rank, int dev, size_t n, size_t bytes) {
     std::lock_guard<std::mutex> lk(mu);
+    std::vector<size_t> idx;
     for (size_t i = 0; i < n; ++i) {
       Slot s;
       s.cap = bytes;
       s.device = dev;
+      s.owner = rank;
+      s.busy = true;  // never handed out by acquire()
+      idx.push_back(slots.size());
       SPK_CUDA(cudaMalloc(&s.ptr, bytes));
       SPK_CUDA(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
       SPK_CUDA(cudaEventCreateWithFlags(&s.freed, cudaEventDisableTiming));
       slots.push_back(s);
     }
+    return idx;
   }
   // A staging buffer of >= bytes on the calling thread's device (caller holds mu).
   size_t acquire(size_t bytes) {
@@ -170,7 +180,11 @@ class LocalTransport final : public Transport {
 
   void send(const void* buf, size_t bytes, int peer, int channel, uint64_t tag, cudaStream_t s) override {
     std::unique_lock<std::mutex> lk(hub_->mu);
-    const size_t i = hub_->acquire(bytes);
+    size_t i;
+    if (!own_.empty() && hub_->slots[own_[next_ % own_.size()]].cap >= bytes)
+      i = own_[next_++ % own_.size()];
+    else
+      i = hub_->acquire(bytes);
     LocalHub::Slot& sl = hub_->slots[i];
     if (sl.used) SPK_CUDA(cudaStreamWaitEvent(s, sl.freed, 0));  // the previous receiver has copied it out
     SPK_CUDA(cudaMemcpyAsync(sl.ptr, buf, bytes, cudaMemcpyDefault, s));
@@ -224,21 +238,27 @@ class LocalTransport final : public Transport {
     SPK_CUDA(cudaStreamWaitEvent(s, sl.ready, 0));
     SPK_CUDA(cudaMemcpyAsync(buf, sl.ptr, bytes, cudaMemcpyDefault, s));
     SPK_CUDA(cudaEventRecord(sl.freed, s));
-    sl.busy = false;
+    if (sl.owner < 0) sl.busy = false;
   }
 
+ public:
+  std::vector<size_t> own_;  // this rank's reserved slots, used in rotation
+  size_t next_ = 0;
+
+ private:
   std::shared_ptr<LocalHub> hub_;
   int rank_;
 };
 
 }  // namespace
 
-std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalHub> hub, int rank) {
-  return std::make_unique<LocalTransport>(std::move(hub), rank);
-}
-
-void local_hub_reserve(const std::shared_ptr<LocalHub>& hub, int device, size_t slots, size_t bytes) {
-  hub->reserve(device, slots, bytes);
+std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalHub> hub, int rank, size_t sends_per_step,
+                                                size_t max_bytes) {
+  int dev = 0;
+  SPK_CUDA(cudaGetDevice(&dev));
+  auto t = std::make_unique<LocalTransport>(hub, rank);
+  if (sends_per_step) t->own_ = hub->reserve(rank, dev, sends_per_step, max_bytes);
+  return t;
 }
 
 }  // namespace spe

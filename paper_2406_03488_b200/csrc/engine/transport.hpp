@@ -55,9 +55,9 @@ std::unique_ptr<Transport> make_nccl_transport(int world, int rank, const std::v
 
 struct LocalHub;
 std::shared_ptr<LocalHub> make_local_hub(int world, double watchdog_seconds);
-std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalHub> hub, int rank);
-// Pre-allocates `slots` staging buffers of `bytes` on `device` (one per message a rank may have
-// in flight: the sends of its comm plan).
-void local_hub_reserve(const std::shared_ptr<LocalHub>& hub, int device, size_t slots, size_t bytes);
+// sends_per_step / max_bytes: the rank's sends of one step (its comm plan); that many staging
+// slots are reserved for it up front and used in rotation (see transport.cpp).
+std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalHub> hub, int rank, size_t sends_per_step = 0,
+                                                size_t max_bytes = 0);
 
 }  // namespace spe

@@ -20,7 +20,13 @@ ap.add_argument("--seq", type=int, default=32768)
 ap.add_argument("--micro", type=int, default=8)
 ap.add_argument("--k", type=int, default=4)
 a = ap.parse_args()
-model, cfg = bench.model_and_cfg(1, a.seq, a.micro, a.k)
+W = bench.WORKLOADS["cfg2"]
+preset, ov = bench.scenario_overrides("cfg2", 1, a.micro, a.k, a.seq)
+cfg = pl.preset_scenario(preset)
+for key, v in ov:
+    pl.apply_scenario_override(cfg, key, str(v))
+model = E.ModelConfig(family=W["family"], dtype=E.BF16, vocab=W["V"], hidden=W["h"], layers=W["L"], heads=W["H"],
+                      head_dim=W["hd"], ffn=W["F"], max_seq=a.seq, seed=42, lr=1e-4, weight_decay=0.0)
 part = pl.cwp_partition(cfg)
 eng = E.Engine(cfg, "seq1f1b", part, model)
 tok = np.random.default_rng(1234).integers(0, model.vocab, size=(cfg.micro_batches, cfg.seq_len + 1)).astype(np.int32)
