@@ -325,6 +325,16 @@ __device__ __forceinline__ void ld_f8(const float* p, float (&f)[8]) {
   f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
 }
 
+// 16-byte global -> shared copies that bypass registers (LDGSTS): the streaming norm kernels
+// prefetch the next row's slice into shared memory while they work on the current one.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 template <int NV, bool RMS>
 __global__ void __launch_bounds__(256) norm_fwd_vec_k(const __nv_bfloat16* __restrict__ x, const float* __restrict__ g,
                                                       __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
@@ -374,96 +384,116 @@ __global__ void __launch_bounds__(256) norm_fwd_vec_k(const __nv_bfloat16* __res
   }
 }
 
-// Rows of h >= 2048 (NV even): two warps per row, each caching half of it (NV/2 16-byte
-// vectors per lane, ~20 registers), so 4 CTAs = 32 warps fit per SM and every load of a
-// row is in flight at once. Each half computes its own mean and centred sum of squares
-// (two passes over registers) and the pair combines them through shared memory in one
-// exchange (Chan: M2 = M2_a + M2_b + (mean_a - mean_b)^2 * H/4), which keeps the
-// two-pass numerics. The one-warp-per-row kernel above held the whole row (128 registers,
-// 16 warps per SM) and reached 0.53 of HBM.
-template <int NV, bool RMS>
-__global__ void __launch_bounds__(256, NV <= 12 ? 4 : (NV <= 16 ? 3 : 2)) norm_fwd_pair_k(const __nv_bfloat16* __restrict__ x,
+// Rows of h >= 2048: G warps per row (G = 2 for h 2048-3072, 4 for h >= 4096), each caching
+// a 1/G slice of the row in registers (NV/G 16-byte vectors per lane). The grid is persistent
+// (3 CTAs per SM striding over rows) and every warp copies its slice of the NEXT row into
+// shared memory (cp.async, no registers) before reducing the current one: the DRAM latency of
+// row r+1 hides behind the reductions, barrier and stores of row r (one row per warp and no
+// prefetch left the HBM pipe idle between waves: 0.52 of HBM). Each slice computes its own
+// mean and centred sum of squares (two passes over registers); the G slices combine them in
+// one shared-memory exchange (Chan: M2 = sum M2_g + (H/G) sum (mean_g - mean)^2).
+template <int NV, int G>
+struct RowSlice {
+  static constexpr int H = 256 * NV, NS = NV / G, RB = 8 / G;  // vectors per lane, rows per CTA
+};
+template <int NV, int G, bool RMS>
+__global__ void __launch_bounds__(256, 3) norm_fwd_rows_k(const __nv_bfloat16* __restrict__ x,
                                                           const float* __restrict__ g, __nv_bfloat16* __restrict__ y,
                                                           float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                           int64_t n, float eps) {
-  constexpr int H = 256 * NV, NH = NV / 2;
-  __shared__ float2 xch[4][2];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, pr = w >> 1, hw = w & 1;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * 4 + pr;
-  const bool ok = row < n;
-  const Bf8* xr = reinterpret_cast<const Bf8*>(x + (ok ? row : 0) * H) + hw * NH * 32;
-  Bf8 xv[NH];
+  using RS = RowSlice<NV, G>;
+  constexpr int H = RS::H, NS = RS::NS;
+  extern __shared__ float4 pf4[];  // [8 warps][NS * 32] Bf8: the next row's slice
+  __shared__ float2 xch[2][RS::RB][G];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, rb = w / G, gi = w % G;
+  Bf8* pf = reinterpret_cast<Bf8*>(pf4) + w * NS * 32;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * RS::RB;
+  int64_t row = static_cast<int64_t>(blockIdx.x) * RS::RB + rb;
+  auto slice = [&](int64_t r) { return reinterpret_cast<const Bf8*>(x + r * H) + gi * NS * 32; };
+  auto prefetch = [&](int64_t r) {
+    const Bf8* xr = slice(r);
 #pragma unroll
-  for (int k = 0; k < NH; ++k) xv[k] = xr[k * 32 + lane];
-  float s = 0.f;
-  if (!RMS) {
+    for (int k = 0; k < NS; ++k) cp_async16(pf + k * 32 + lane, xr + k * 32 + lane);
+    cp_async_commit();
+  };
+  if (row < n) prefetch(row);
+  const float* gs = g + gi * (H / G);
+  for (int par = 0; row < n; row += stride, par ^= 1) {
+    Bf8 cur[NS];
+    cp_async_wait_all();
 #pragma unroll
-    for (int k = 0; k < NH; ++k) {
-      float f[8];
-      bf8_to_f(xv[k], f);
+    for (int k = 0; k < NS; ++k) cur[k] = pf[k * 32 + lane];  // own lane's chunks: no barrier
+    if (row + stride < n) prefetch(row + stride);
+    float sm = 0.f;
+    if (!RMS) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) s += f[e];
+      for (int k = 0; k < NS; ++k) {
+        float f[8];
+        bf8_to_f(cur[k], f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sm += f[e];
+      }
+      sm = warp_sum(sm);
     }
-    s = warp_sum(s);
-  }
-  const float mh = RMS ? 0.f : s * (2.f / H);  // this half's mean
-  float ss = 0.f;
+    const float mg = RMS ? 0.f : sm * (static_cast<float>(G) / H);  // this slice's mean
+    float ss = 0.f;
 #pragma unroll
-  for (int k = 0; k < NH; ++k) {
-    float f[8];
-    bf8_to_f(xv[k], f);
+    for (int k = 0; k < NS; ++k) {
+      float f[8];
+      bf8_to_f(cur[k], f);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) ss += (f[e] - mh) * (f[e] - mh);
-  }
-  ss = warp_sum(ss);
-  if (lane == 0) xch[pr][hw] = make_float2(mh, ss);
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + pr) : "memory");
-  const float2 o = xch[pr][hw ^ 1];
-  const float mean = RMS ? 0.f : 0.5f * (mh + o.x);
-  const float d = mh - o.x;
-  const float rstd = rsqrtf((ss + o.y + (RMS ? 0.f : d * d * (H / 4))) / H + eps);
-  if (!ok) return;
-  Bf8* yr = reinterpret_cast<Bf8*>(y + row * H) + hw * NH * 32;
-  const float* gh = g + hw * (H / 2);
+      for (int e = 0; e < 8; ++e) ss += (f[e] - mg) * (f[e] - mg);
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) xch[par][rb][gi] = make_float2(mg, ss);
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + rb), "r"(32 * G) : "memory");
+    float mean = 0.f, m2 = 0.f;
 #pragma unroll
-  for (int k = 0; k < NH; ++k) {
-    float f[8], gv[8];
-    bf8_to_f(xv[k], f);
-    ld_f8(gh + (k * 32 + lane) * 8, gv);
+    for (int q = 0; q < G; ++q) mean += xch[par][rb][q].x;
+    mean *= 1.f / G;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) f[e] = (f[e] - mean) * rstd * gv[e];
-    yr[k * 32 + lane] = f_to_bf8(f);
-  }
-  if (lane == 0 && hw == 0) {
-    if (!RMS) mean_out[row] = mean;
-    rstd_out[row] = rstd;
+    for (int q = 0; q < G; ++q) {
+      const float2 o = xch[par][rb][q];
+      m2 += o.y + (RMS ? 0.f : (o.x - mean) * (o.x - mean) * (H / G));
+    }
+    if (RMS) mean = 0.f;
+    const float rstd = rsqrtf(m2 / H + eps);
+    Bf8* yr = reinterpret_cast<Bf8*>(y + row * H) + gi * NS * 32;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      float f[8], gv[8];
+      bf8_to_f(cur[k], f);
+      ld_f8(gs + (k * 32 + lane) * 8, gv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = (f[e] - mean) * rstd * gv[e];
+      yr[k * 32 + lane] = f_to_bf8(f);
+    }
+    if (lane == 0 && gi == 0) {
+      if (!RMS) mean_out[row] = mean;
+      rstd_out[row] = rstd;
+    }
   }
 }
 
+// y = (x - mean) * rstd * g: no reduction, so a flat grid-stride loop over 16-byte chunks
+// (the MLP activation's access pattern, ~0.9 of HBM) instead of one row per warp.
 template <int NV, bool RMS>
-__global__ void __launch_bounds__(256, 4) norm_apply_vec_k(const __nv_bfloat16* __restrict__ x, const float* __restrict__ g,
+__global__ void __launch_bounds__(256) norm_apply_vec_k(const __nv_bfloat16* __restrict__ x, const float* __restrict__ g,
                                                         const float* __restrict__ mean, const float* __restrict__ rstd,
                                                         __nv_bfloat16* __restrict__ y, int64_t n) {
-  constexpr int H = 256 * NV;
-  const int lane = threadIdx.x & 31;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + threadIdx.x / 32;
-  if (row >= n) return;
-  const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
-  const Bf8* xr = reinterpret_cast<const Bf8*>(x + row * H);
-  Bf8* yr = reinterpret_cast<Bf8*>(y + row * H);
-  // every 16-byte load of the row in flight at once (one DRAM round trip per row; issued
-  // per chunk inside the output loop they were ten dependent round trips)
-  Bf8 xv[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) xv[k] = xr[k * 32 + lane];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
+  constexpr int PER_ROW = 32 * NV;  // 16-byte chunks per row
+  const int64_t chunks = n * PER_ROW;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < chunks;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / PER_ROW;
+    const int c = static_cast<int>(i - row * PER_ROW);
+    const float mu = RMS ? 0.f : __ldg(mean + row), rs = __ldg(rstd + row);
     float f[8], gv[8];
-    bf8_to_f(xv[k], f);
-    ld_f8(g + (k * 32 + lane) * 8, gv);
+    bf8_to_f(reinterpret_cast<const Bf8*>(x)[i], f);
+    ld_f8(g + c * 8, gv);
 #pragma unroll
     for (int e = 0; e < 8; ++e) f[e] = (f[e] - mu) * rs * gv[e];
-    yr[k * 32 + lane] = f_to_bf8(f);
+    reinterpret_cast<Bf8*>(y)[i] = f_to_bf8(f);
   }
 }
 
@@ -547,48 +577,64 @@ __global__ void __launch_bounds__(256) norm_bwd_vec_k(const __nv_bfloat16* __res
   }
 }
 
-// Wide rows (NV >= 8, h >= 2048): two warps per row, each owning one half of the
-// columns (NV/2 16-byte vectors per lane, cached in registers). Half the registers
-// of norm_bwd_vec_k, so two 8-warp CTAs fit per SM and each row's load latency
-// is split over two warps; the row sums are combined through shared memory.
-template <int NV, bool RMS>
-__global__ void __launch_bounds__(256, 2) norm_bwd_pair_k(const __nv_bfloat16* __restrict__ dy,
+// Backward of the same row layout (G warps per row, persistent grid, next row's x / dy slice
+// prefetched during the current row; the residual gradient is loaded at the top of the row's
+// iteration so its latency hides behind the two reductions). dg partials: one shared-memory
+// row of H/G floats per warp (no atomics), summed over the CTA's rows and added once.
+template <int NV, int G, bool RMS>
+__global__ void __launch_bounds__(256, 2) norm_bwd_rows_k(const __nv_bfloat16* __restrict__ dy,
                                                           const __nv_bfloat16* __restrict__ x,
                                                           const float* __restrict__ g, const float* __restrict__ mean,
                                                           const float* __restrict__ rstd, const __nv_bfloat16* dres,
                                                           __nv_bfloat16* dx, float* __restrict__ dg, int64_t n) {
-  constexpr int H = 256 * NV, NH = NV / 2, HH = H / 2;
-  extern __shared__ float4 sdg4[];  // [8 warps][H/2] fp32 dgain partials, then [2 parity][4 pairs][2 halves][2]
+  using RS = RowSlice<NV, G>;
+  constexpr int H = RS::H, NS = RS::NS, HS = H / G;
+  // [8 warps][H/G] fp32 dgain partials, then [8 warps][2][NS * 32] Bf8: next row's x / dy slices
+  extern __shared__ float4 sdg4[];
   float* sdg = reinterpret_cast<float*>(sdg4);
-  float* xch = sdg + 8 * HH;
-  const int lane = threadIdx.x & 31, w = threadIdx.x / 32, pr = w >> 1, hw = w & 1;
-  float* my = sdg + w * HH;
-  for (int c = lane * 4; c < HH; c += 128) *reinterpret_cast<float4*>(my + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+  __shared__ float2 xch[2][RS::RB][G];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, rb = w / G, gi = w % G;
+  float* my = sdg + w * HS;
+  Bf8* pfx = reinterpret_cast<Bf8*>(sdg + 8 * HS) + w * 2 * NS * 32;
+  Bf8* pfd = pfx + NS * 32;
+  for (int c = lane * 4; c < HS; c += 128) *reinterpret_cast<float4*>(my + c) = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncwarp();
-  int par = 0;
-  for (int64_t row = static_cast<int64_t>(blockIdx.x) * 4 + pr; row < n;
-       row += static_cast<int64_t>(gridDim.x) * 4, par ^= 1) {
-    const Bf8* xr = reinterpret_cast<const Bf8*>(x + row * H) + hw * NH * 32;
-    const Bf8* dyr = reinterpret_cast<const Bf8*>(dy + row * H) + hw * NH * 32;
-    const float* gh = g + hw * HH;
-    const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
-    const Bf8* drr = dres ? reinterpret_cast<const Bf8*>(dres + row * H) + hw * NH * 32 : nullptr;
-    // the residual gradient is loaded with x and dy (one DRAM round trip per row; loaded in
-    // the output pass it was a second, dependent one)
-    Bf8 xv[NH], dv[NH], rv[NH];
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * RS::RB;
+  int64_t row = static_cast<int64_t>(blockIdx.x) * RS::RB + rb;
+  auto sl = [&](const __nv_bfloat16* base, int64_t r) { return reinterpret_cast<const Bf8*>(base + r * H) + gi * NS * 32; };
+  auto prefetch = [&](int64_t r) {
+    const Bf8 *xr = sl(x, r), *dyr = sl(dy, r);
 #pragma unroll
-    for (int k = 0; k < NH; ++k) {
-      xv[k] = xr[k * 32 + lane];
-      dv[k] = dyr[k * 32 + lane];
-      if (drr) rv[k] = drr[k * 32 + lane];
+    for (int k = 0; k < NS; ++k) {
+      cp_async16(pfx + k * 32 + lane, xr + k * 32 + lane);
+      cp_async16(pfd + k * 32 + lane, dyr + k * 32 + lane);
     }
+    cp_async_commit();
+  };
+  if (row < n) prefetch(row);
+  const float* gs = g + gi * HS;
+  for (int par = 0; row < n; row += stride, par ^= 1) {
+    Bf8 xv[NS], dv[NS], rv[NS];
+    if (dres) {  // residual gradient: its latency hides behind the two reductions
+      const Bf8* rr = sl(dres, row);
+#pragma unroll
+      for (int k = 0; k < NS; ++k) rv[k] = rr[k * 32 + lane];
+    }
+    cp_async_wait_all();
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      xv[k] = pfx[k * 32 + lane];
+      dv[k] = pfd[k * 32 + lane];
+    }
+    if (row + stride < n) prefetch(row + stride);
+    const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < NH; ++k) {
+    for (int k = 0; k < NS; ++k) {
       float f[8], d[8], gv[8];
       bf8_to_f(xv[k], f);
       bf8_to_f(dv[k], d);
-      ld_f8(gh + (k * 32 + lane) * 8, gv);
+      ld_f8(gs + (k * 32 + lane) * 8, gv);
       float* acc = my + (k * 32 + lane) * 8;
       float4 a0 = *reinterpret_cast<float4*>(acc), a1 = *reinterpret_cast<float4*>(acc + 4);
       float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
@@ -604,37 +650,38 @@ __global__ void __launch_bounds__(256, 2) norm_bwd_pair_k(const __nv_bfloat16* _
     }
     s1 = RMS ? 0.f : warp_sum(s1);
     s2 = warp_sum(s2);
-    float* slot = xch + ((par * 4 + pr) * 2) * 2;
-    if (lane == 0) {
-      slot[hw * 2] = s1;
-      slot[hw * 2 + 1] = s2;
-    }
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + pr) : "memory");
-    const float m1 = RMS ? 0.f : (s1 + slot[(hw ^ 1) * 2]) / H;
-    const float m2 = (s2 + slot[(hw ^ 1) * 2 + 1]) / H;
-    Bf8* dxr = reinterpret_cast<Bf8*>(dx + row * H) + hw * NH * 32;
+    if (lane == 0) xch[par][rb][gi] = make_float2(s1, s2);
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + rb), "r"(32 * G) : "memory");
+    float t1 = 0.f, t2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < NH; ++k) {
+    for (int q = 0; q < G; ++q) {
+      t1 += xch[par][rb][q].x;
+      t2 += xch[par][rb][q].y;
+    }
+    const float m1 = RMS ? 0.f : t1 / H, m2 = t2 / H;
+    Bf8* dxr = reinterpret_cast<Bf8*>(dx + row * H) + gi * NS * 32;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
       float f[8], d[8], gv[8], r[8];
       bf8_to_f(xv[k], f);
       bf8_to_f(dv[k], d);
-      ld_f8(gh + (k * 32 + lane) * 8, gv);
-      if (drr) bf8_to_f(rv[k], r);
+      ld_f8(gs + (k * 32 + lane) * 8, gv);
+      if (dres) bf8_to_f(rv[k], r);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const float xh = (f[e] - mu) * rs;
-        f[e] = rs * (d[e] * gv[e] - m1 - xh * m2) + (drr ? r[e] : 0.f);
+        f[e] = rs * (d[e] * gv[e] - m1 - xh * m2) + (dres ? r[e] : 0.f);
       }
       dxr[k * 32 + lane] = f_to_bf8(f);
     }
   }
   __syncthreads();
   for (int c = threadIdx.x; c < H; c += 256) {
-    const int h2 = c / HH, cc = c - h2 * HH;
-    float s = 0.f;
+    const int q = c / HS, cc = c - q * HS;
+    float acc = 0.f;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) s += sdg[(q * 2 + h2) * HH + cc];
-    atomicAdd(&dg[c], s);
+    for (int r = 0; r < RS::RB; ++r) acc += sdg[(r * G + q) * HS + cc];
+    atomicAdd(&dg[c], acc);
   }
 }
 
@@ -827,11 +874,14 @@ void norm_fwd(DType t, bool rms, const void* x, const float* g, void* y, float* 
         const auto* xb = static_cast<const __nv_bfloat16*>(x);
         auto* yb = static_cast<__nv_bfloat16*>(y);
         if constexpr (NV >= 8 && NV % 2 == 0) {
-          const unsigned grid = static_cast<unsigned>((n + 3) / 4);
+          constexpr int G = NV >= 16 ? 4 : 2;
+          const int64_t blocks = (n + 8 / G - 1) / (8 / G);
+          const unsigned grid = static_cast<unsigned>(std::min<int64_t>(blocks, 3 * num_sms()));
+          const size_t pf = 8 * (NV / G) * 32 * 16;  // next-row slices, [8 warps][NS * 32] x 16 B
           if (rms)
-            norm_fwd_pair_k<NV, true><<<grid, 256, 0, s>>>(xb, g, yb, mean, rstd, n, eps);
+            norm_fwd_rows_k<NV, G, true><<<grid, 256, pf, s>>>(xb, g, yb, mean, rstd, n, eps);
           else
-            norm_fwd_pair_k<NV, false><<<grid, 256, 0, s>>>(xb, g, yb, mean, rstd, n, eps);
+            norm_fwd_rows_k<NV, G, false><<<grid, 256, pf, s>>>(xb, g, yb, mean, rstd, n, eps);
           return;
         }
         const unsigned grid = static_cast<unsigned>((n + 7) / 8);
@@ -857,7 +907,7 @@ void norm_apply(DType t, bool rms, const void* x, const float* g, const float* m
   if (n == 0) return;
   if (t == DType::kBF16 && dispatch_nv(h, [&](auto nv) {
         constexpr int NV = decltype(nv)::value;
-        const unsigned grid = static_cast<unsigned>((n + 7) / 8);
+        const unsigned grid = static_cast<unsigned>(stream_grid(n * 32 * NV, 256));
         const auto* xb = static_cast<const __nv_bfloat16*>(x);
         auto* yb = static_cast<__nv_bfloat16*>(y);
         if (rms)
@@ -890,27 +940,22 @@ void norm_bwd(DType t, bool rms, const void* dy, const void* x, const float* g, 
           kern<<<grid, 256, sm, s>>>(static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), g, mean,
                                      rstd, static_cast<const __nv_bfloat16*>(dres), static_cast<__nv_bfloat16*>(dx), dg, n);
         };
-        if constexpr (NV >= 8 && NV <= 12 && NV % 2 == 0) {  // measured: +5 % at h 2560, -8 % at h 4096
-          static const bool pair = [] {
-            const char* e = std::getenv("SP_NORM_BWD_PAIR");  // tuning: 0 = one warp per row
-            return e ? std::atoi(e) != 0 : true;
-          }();
-          if (pair) {
-            const size_t sm2 = sizeof(float) * (8 * 128 * NV + 32);
-            const int64_t b2 = (n + 3) / 4;
-            const unsigned grid2 = static_cast<unsigned>(b2 < 2 * num_sms() ? b2 : 2 * num_sms());
-            auto launch2 = [&](auto kern) {
-              SPK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-              kern<<<grid2, 256, sm2, s>>>(static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), g,
-                                          mean, rstd, static_cast<const __nv_bfloat16*>(dres),
-                                          static_cast<__nv_bfloat16*>(dx), dg, n);
-            };
-            if (rms)
-              launch2(norm_bwd_pair_k<NV, true>);
-            else
-              launch2(norm_bwd_pair_k<NV, false>);
-            return;
-          }
+        if constexpr (NV >= 8 && NV % 2 == 0) {  // G warps per row, persistent, next row prefetched
+          constexpr int G = NV >= 16 ? 4 : 2;
+          const size_t sm2 = sizeof(float) * 8 * (256 * NV / G) + 8 * 2 * (NV / G) * 32 * 16;
+          const int64_t b2 = (n + 8 / G - 1) / (8 / G);
+          const unsigned grid2 = static_cast<unsigned>(std::min<int64_t>(b2, 2 * num_sms()));
+          auto launch2 = [&](auto kern) {
+            SPK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+            kern<<<grid2, 256, sm2, s>>>(static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), g,
+                                        mean, rstd, static_cast<const __nv_bfloat16*>(dres),
+                                        static_cast<__nv_bfloat16*>(dx), dg, n);
+          };
+          if (rms)
+            launch2(norm_bwd_rows_k<NV, G, true>);
+          else
+            launch2(norm_bwd_rows_k<NV, G, false>);
+          return;
         }
         if (rms)
           launch(norm_bwd_vec_k<NV, true>);

@@ -13,9 +13,7 @@
 // all run on this one kernel without transposes.
 #include <cudaTypedefs.h>
 
-#include <algorithm>
 #include <cstdlib>
-#include <map>
 #include <mutex>
 
 #include "cuda/common.cuh"
@@ -37,11 +35,6 @@ struct __align__(64) TcParams {
   GemmArgs g;
   int a_mn, b_mn;
   int num_m_blk, num_n_blk, num_k_blk;
-  // 2-CTA kernel, tail split (see gemm_tc2_k): tiles >= full_tiles are split into split_c
-  // K-chunks of kb_per K blocks; partials go to ws, cnt counts arrivals per (tail tile, CTA).
-  int full_tiles = 0, split_c = 1, kb_per = 0;
-  float* ws = nullptr;
-  unsigned* cnt = nullptr;
 };
 
 template <typename TC>
@@ -284,32 +277,6 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
-// Work items of the 2-CTA kernel. Tiles [0, full_tiles) fill whole waves of the persistent
-// grid and run over all of K. The R < ncl/2 tiles of the last, partial wave would leave most
-// CTA pairs idle (o-proj / MLP-down at N = 2560: 400 tiles = 5.4 waves of 74 pairs; the
-// o-proj weight gradient 100 tiles = 1.35 waves), so each is split into split_c K-chunks that
-// run on different pairs. Every chunk stores its fp32 partial in a workspace slot; the last
-// chunk of a tile to arrive (per-CTA counter) sums all slots in chunk order -- deterministic
-// regardless of arrival order -- and runs the normal epilogue on the sum.
-struct Item {
-  int tile, kb0, kb1, tail, chunk;
-};
-__device__ __forceinline__ int num_items(const TcParams& p) {
-  const int tiles = p.num_m_blk * p.num_n_blk;
-  return p.split_c > 1 ? p.full_tiles + (tiles - p.full_tiles) * p.split_c : tiles;
-}
-__device__ __forceinline__ Item item_of(const TcParams& p, int it) {
-  if (p.split_c <= 1 || it < p.full_tiles) return Item{it, 0, p.num_k_blk, -1, 0};
-  const int t = (it - p.full_tiles) / p.split_c, j = (it - p.full_tiles) - t * p.split_c;
-  const int kb0 = j * p.kb_per;
-  return Item{p.full_tiles + t, kb0, min(p.num_k_blk, kb0 + p.kb_per), t, j};
-}
-__device__ __forceinline__ float4 ld_cg_f4(const float* ptr) {
-  float4 v;
-  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr));
-  return v;
-}
-
 template <typename TC>
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc2_k(const __grid_constant__ TcParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -347,18 +314,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc2_k(const __grid_consta
   tc::tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
-  const int n_items = num_items(p);  // 256 x 256 tiles (or K-chunks of the tail tiles)
+  const int num_tiles = p.num_m_blk * p.num_n_blk;  // 256 x 256 tiles
   if (warp == 0) {
     if (lane == 0) {
       tc::tma_prefetch(&p.tma_a);
       tc::tma_prefetch(&p.tma_b);
       int stage = 0;
       uint32_t phase = 0;
-      for (int item = cid; item < n_items; item += ncl) {
-        const Item w = item_of(p, item);
-        const int mb = w.tile % p.num_m_blk, nb = w.tile / p.num_m_blk;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
         const int m0 = mb * 256 + static_cast<int>(rank) * BM2, n0 = nb * 256 + static_cast<int>(rank) * BNH;
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+        for (int kb = 0; kb < p.num_k_blk; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t bar = mapa_rank0(tc::smem_u32(&full[stage]));
           if (rank == 0) tc::mbar_expect_tx(&full[stage], 2 * STAGE2_BYTES);
@@ -389,12 +355,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc2_k(const __grid_consta
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int item = cid; item < n_items; item += ncl) {
-        const Item w = item_of(p, item);
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
         tc::mbar_wait_w(&tempty[acc], acc_phase ^ 1);
         tc::tc_fence_after();
         const uint32_t d = tmem_base + acc * 256;
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+        for (int kb = 0; kb < p.num_k_blk; ++kb) {
           tc::mbar_wait_w(&full[stage], phase);
           tc::tc_fence_after();
           const uint32_t a_base = tc::smem_u32(sA + stage * A2_BYTES), b_base = tc::smem_u32(sB + stage * B2_BYTES);
@@ -404,7 +369,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc2_k(const __grid_consta
                                        : tc::smem_desc(a_base + kk * 32, 16, 1024, tc::kSwizzle128B);
             const uint64_t bd = p.b_mn ? tc::smem_desc(b_base + kk * 2048, 8192, 1024, tc::kSwizzle128B)
                                        : tc::smem_desc(b_base + kk * 32, 16, 1024, tc::kSwizzle128B);
-            const uint32_t accum = (kb != w.kb0 || kk != 0) ? 1u : 0u;
+            const uint32_t accum = (kb | kk) != 0;
             asm volatile(
                 "{\n\t.reg .pred p, e;\n\t"
                 "elect.sync _|e, 0xffffffff;\n\t"
@@ -438,82 +403,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc2_k(const __grid_consta
     }
   } else {
     const int quarter = warp % 4;  // TMEM lane quarter this warp may access
-    volatile unsigned* last_flag = tmem_slot + 1;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int item = cid; item < n_items; item += ncl) {
-      const Item w = item_of(p, item);
-      const int mb = w.tile % p.num_m_blk, nb = w.tile / p.num_m_blk;
+    for (int tile = cid; tile < num_tiles; tile += ncl) {
+      const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::tc_fence_after();
-      const int rl = quarter * 32 + lane;  // row within this CTA's 128-row half
-      const int64_t row = (int64_t)mb * 256 + rank * BM2 + rl;
-      if (w.tail < 0) {
+      const int64_t row = (int64_t)mb * 256 + rank * BM2 + quarter * 32 + lane;
 #pragma unroll 1
-        for (int c0 = 0; c0 < 256; c0 += 32) {
-          const int64_t col0 = (int64_t)nb * 256 + c0;
-          uint32_t r[32];
-          tc::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 256 + c0, r);
-          tc::tmem_ld_wait();
-          if (row < p.g.M && col0 < p.g.N) store_chunk<TC>(p.g, row, col0, r);
-        }
-      } else {  // K-chunk of a tail tile: fp32 partial -> workspace slot (tail, chunk, CTA)
-        float* slot = p.ws + ((static_cast<size_t>(w.tail) * p.split_c + w.chunk) * 2 + rank) * (128 * 256) + rl * 256;
-#pragma unroll 1
-        for (int c0 = 0; c0 < 256; c0 += 32) {
-          uint32_t r[32];
-          tc::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 256 + c0, r);
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            reinterpret_cast<float4*>(slot + c0)[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                                                                  __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-        }
+      for (int c0 = 0; c0 < 256; c0 += 32) {
+        const int64_t col0 = (int64_t)nb * 256 + c0;
+        uint32_t r[32];
+        tc::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * 256 + c0, r);
+        tc::tmem_ld_wait();
+        if (row < p.g.M && col0 < p.g.N) store_chunk<TC>(p.g, row, col0, r);
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(mapa_rank0(tc::smem_u32(&tempty[acc])));
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-      if (w.tail >= 0) {
-        // publish the partial, count this chunk; the tile's last chunk reduces all of them
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 2 && lane == 0) {
-          unsigned* c = p.cnt + w.tail * 2 + rank;
-          const unsigned prev = atomicAdd(c, 1u);
-          const bool last = prev == static_cast<unsigned>(p.split_c - 1);
-          if (last) *c = 0u;  // ready for the next launch (graph replays included)
-          *last_flag = last ? 1u : 0u;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (*last_flag) {
-          __threadfence();
-          const float* base = p.ws + (static_cast<size_t>(w.tail) * p.split_c * 2 + rank) * (128 * 256) + rl * 256;
-#pragma unroll 1
-          for (int c0 = 0; c0 < 256; c0 += 32) {
-            const int64_t col0 = (int64_t)nb * 256 + c0;
-            float v[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = 0.f;
-            for (int j = 0; j < p.split_c; ++j) {  // fixed chunk order: deterministic sum
-              const float* src = base + static_cast<size_t>(j) * 2 * (128 * 256) + c0;
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const float4 f = ld_cg_f4(src + 4 * q);
-                v[4 * q] += f.x;
-                v[4 * q + 1] += f.y;
-                v[4 * q + 2] += f.z;
-                v[4 * q + 3] += f.w;
-              }
-            }
-            uint32_t r[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(v[e]);
-            if (row < p.g.M && col0 < p.g.N) store_chunk<TC>(p.g, row, col0, r);
-          }
-        }
-      }
     }
   }
   tc::tc_fence_before();
@@ -550,62 +459,6 @@ void make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
-constexpr int kMaxSplit = 8;
-// Workspace of the tail split per (device, stream): fp32 partial tiles + arrival counters
-// (zeroed once; the last chunk of every tile resets its counter, so graph replays reuse it).
-// Per stream because GEMMs of different streams (the weight-gradient side stream) run
-// concurrently; GEMMs of one stream are ordered. Grown only outside stream capture: a launch
-// that would need to grow it while its stream is being captured runs unsplit.
-struct SplitWs {
-  float* ws = nullptr;
-  unsigned* cnt = nullptr;
-  size_t cap = 0;
-  int cnt_cap = 0;
-  bool ensure(size_t floats, int counters, cudaStream_t s) {
-    if (floats <= cap && counters <= cnt_cap) return true;
-    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) {
-      cudaGetLastError();
-      return false;
-    }
-    const size_t f = std::max(floats, cap), n = static_cast<size_t>(std::max(counters, cnt_cap));
-    float* nw = nullptr;
-    unsigned* nc = nullptr;
-    if (cudaMalloc(&nw, f * sizeof(float)) != cudaSuccess || cudaMalloc(&nc, n * sizeof(unsigned)) != cudaSuccess ||
-        cudaMemsetAsync(nc, 0, n * sizeof(unsigned), s) != cudaSuccess) {
-      cudaGetLastError();
-      if (nw) cudaFree(nw);
-      if (nc) cudaFree(nc);
-      return false;
-    }
-    if (ws) {  // the previous buffers may still be read by launches queued on s
-      SPK_CUDA(cudaStreamSynchronize(s));
-      cudaFree(ws);
-      cudaFree(cnt);
-    }
-    ws = nw;
-    cnt = nc;
-    cap = f;
-    cnt_cap = static_cast<int>(n);
-    return true;
-  }
-};
-SplitWs& split_ws(cudaStream_t s) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, SplitWs> per;
-  int dev = 0;
-  SPK_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lk(mu);
-  return per[{dev, s}];
-}
-bool tail_split_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("SP_GEMM_TAIL_SPLIT");  // tuning: 0 = no tail split
-    return e ? std::atoi(e) != 0 : true;
-  }();
-  return on;
-}
 
 }  // namespace
 
@@ -649,25 +502,6 @@ void gemm_tcgen05(const GemmArgs& a, cudaStream_t s) {
     p.num_n_blk = static_cast<int>((a.N + 255) / 256);
     p.num_k_blk = static_cast<int>((a.K + BK2 - 1) / BK2);
     const int pairs = static_cast<int>(tiles2 < num_sms() / 2 ? tiles2 : num_sms() / 2);
-    // Tail split: the R tiles of a partial last wave (R <= pairs / 2) become c K-chunks each.
-    {
-      const int tiles = static_cast<int>(tiles2), R = tiles % pairs;
-      int c = R > 0 ? pairs / R : 1;
-      c = std::min({c, p.num_k_blk / 2, kMaxSplit});
-      if (R > 0 && c >= 2 && tail_split_enabled()) {
-        const int kb_per = (p.num_k_blk + c - 1) / c;
-        c = (p.num_k_blk + kb_per - 1) / kb_per;  // every chunk gets >= 1 K block
-        SplitWs& w = split_ws(s);
-        const size_t need = static_cast<size_t>(R) * c * 2 * 128 * 256;
-        if (c >= 2 && w.ensure(need, R * 2, s)) {
-          p.full_tiles = tiles - R;
-          p.split_c = c;
-          p.kb_per = kb_per;
-          p.ws = w.ws;
-          p.cnt = w.cnt;
-        }
-      }
-    }
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(2 * pairs);
     lc.blockDim = dim3(NUM_THREADS);

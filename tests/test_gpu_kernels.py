@@ -32,12 +32,9 @@ def _rel(a, b):
                                    (10170, 7680, 2560),
                                    # weight-gradient shapes (few tiles, long K)
                                    (2560, 2560, 6674), (7680, 2560, 8496), (300, 520, 4100),
-                                   (10170, 2560, 2560)])  # o-proj: 400 tiles -> the 30-tile tail is K-split
+                                   (10170, 2560, 2560)])  # o-proj: 400 tiles of 256 x 256, a partial last wave
 def test_tcgen05_gemm_layouts(gpu, a_k, b_k, M, N, K):
-    """All operand majorness combinations and epilogues vs fp64. Several shapes leave a partial
-    last wave of 256x256 tiles that the 2-CTA kernel splits along K (e.g. 2048x2560: 80 tiles
-    = 74 + 6 -> 8 chunks each; 10170x2560: 400 = 5 x 74 + 30 -> 2); the split result must be
-    bit-identical run to run (fixed-order reduction)."""
+    """All operand majorness combinations and epilogues vs fp64; results bit-identical run to run."""
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
     A = torch.randn((M, K) if a_k else (K, M), device="cuda", generator=g).to(torch.bfloat16)
     B = torch.randn((N, K) if b_k else (K, N), device="cuda", generator=g).to(torch.bfloat16)
@@ -56,7 +53,7 @@ def test_tcgen05_gemm_layouts(gpu, a_k, b_k, M, N, K):
     assert _rel(out, ref) < tol32, _rel(out, ref)
     again = torch.empty_like(out)
     _gemm(2, A, a_k, B, b_k, again, 1, 0, M, N, K)
-    assert torch.equal(out, again)  # deterministic, tail split included
+    assert torch.equal(out, again)  # deterministic
     outb = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     _gemm(2, A, a_k, B, b_k, outb, 0, 0, M, N, K)
     assert _rel(outb.float(), ref) < 8e-3

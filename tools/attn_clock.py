@@ -12,8 +12,14 @@ import pynvml  # noqa: E402
 import torch  # noqa: E402
 from paper_2406_03488_b200 import _capi  # noqa: E402
 
-which = sys.argv[1] if len(sys.argv) > 1 else "bwd"
-n, q_off, H, hd = (int(x) for x in (sys.argv[2:6] if len(sys.argv) > 5 else (6674, 26094, 32, 80)))
+args = sys.argv[1:]
+variant = None
+if args[:1] == ["--variant"]:  # a tuning build from tools/build_variant.py
+    variant = args[1]
+    _capi.LIB_PATH = _capi.LIB_PATH.parent / "variants" / f"libseqpipe_b200_{variant}.so"
+    args = args[2:]
+which = args[0] if args else "bwd"
+n, q_off, H, hd = (int(x) for x in (args[1:5] if len(args) > 4 else (6674, 26094, 32, 80)))
 h, L = H * hd, q_off + n
 q = torch.randn(n, h, device="cuda").to(torch.bfloat16)
 kv = torch.randn(L, 2 * h, device="cuda").to(torch.bfloat16)
@@ -74,5 +80,5 @@ for x in samples:
     reasons |= x[2]
 ms = e0.elapsed_time(e1) / reps
 fl = 4 * H * hd * (n * q_off + n * n / 2) * (1 if which == "fwd" else 2)
-print(f"{which}: {ms:.3f} ms/call  {fl / ms / 1e9:.0f} TF algorithmic  sm_mhz median {clk[len(clk) // 2]} "
+print(f"{variant or 'product'} {which}: {ms:.3f} ms/call  {fl / ms / 1e9:.0f} TF algorithmic  sm_mhz median {clk[len(clk) // 2]} "
       f"(min {clk[0]} max {clk[-1]})  power median {pw[len(pw) // 2]:.0f} W  reasons 0x{reasons:x}")
