@@ -1301,10 +1301,10 @@ void attn_fwd_tc(const void* q, const void* kv, void* o, float* lse, int64_t n, 
   p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(hd));
   auto run = [&](auto hd_tag) {
     constexpr int HD = decltype(hd_tag)::value;
+    dim3 grid(static_cast<unsigned>(((n + BQ - 1) / BQ + 1) / 2), static_cast<unsigned>(H));  // query-tile pairs
     constexpr size_t smem = fwd_smem<HD>();
     static_assert(smem <= 232448, "attention fwd smem");
     SPK_CUDA(cudaFuncSetAttribute(attn_fwd_tc_k<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 grid(static_cast<unsigned>(((n + BQ - 1) / BQ + 1) / 2), static_cast<unsigned>(H));  // query-tile pairs
     attn_fwd_tc_k<HD><<<grid, 640, smem, s>>>(p);
     SPK_LAUNCH_CHECK();
   };

@@ -1,9 +1,11 @@
 #!/usr/bin/env python
 """HBM roofline of the bf16 elementwise kernels at the bench shapes, through the C-ABI:
 norm fwd / bwd (+ residual gradient) and the MLP activation fwd / bwd. CUDA events around
-single launches, L2 flushed before each (256 MB write), median of 15. Algorithmic bytes =
-tensors read + written once; fraction against MEASURED_PEAKS.json hbm_gbs.
-tools/elem_bench.py [n] [h] [F]"""
+single launches, median of 15, L2 flushed before each by READING a 256 MB buffer (a write
+flush leaves ~126 MB of dirty lines whose write-back lands inside the next kernel: the
+round-2 numbers taken that way are ~30 % low for these ~100 MB kernels; SP_FLUSH=write
+reproduces them). Algorithmic bytes = tensors read + written once; fraction against
+MEASURED_PEAKS.json hbm_gbs. tools/elem_bench.py [n] [h] [F]"""
 import ctypes as C
 import json
 import sys
@@ -23,7 +25,9 @@ except Exception:  # noqa: BLE001
 lib = _capi.lib()
 P = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
 s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+import os  # noqa: E402
+flush = torch.ones(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB
+FLUSH_WRITE = os.environ.get("SP_FLUSH", "read") == "write"
 
 
 def timed(fn, reps=15):
@@ -31,7 +35,10 @@ def timed(fn, reps=15):
         fn()
     ts = []
     for _ in range(reps):
-        flush.fill_(1)
+        if FLUSH_WRITE:
+            flush.fill_(1.0)
+        else:
+            flush.sum()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
@@ -71,6 +78,7 @@ cases = [
 ]
 for name, fn, byts in cases:
     t = timed(fn)
-    print(json.dumps({"kernel": name, "n": n, "h": h, "F": F, "us": round(t * 1e6, 1),
+    print(json.dumps({"kernel": name, "flush": "write" if FLUSH_WRITE else "read", "n": n, "h": h, "F": F,
+                      "us": round(t * 1e6, 1),
                       "algorithmic_MB": round(byts / 1e6, 1), "GBps": round(byts / t / 1e9),
                       "frac_of_hbm": round(byts / t / 1e9 / HBM, 3)}), flush=True)

@@ -33,7 +33,8 @@ from paper_2406_03488_b200 import engine as E  # noqa: E402
 from paper_2406_03488_b200 import planner as pl  # noqa: E402
 
 MODELS = {"gpt-2.7b": dict(family=E.GPT, vocab=50257, hidden=2560, heads=32, head_dim=80, ffn=10240),
-          "llama-7b": dict(family=E.LLAMA, vocab=32000, hidden=4096, heads=32, head_dim=128, ffn=11008)}
+          "llama-7b": dict(family=E.LLAMA, vocab=32000, hidden=4096, heads=32, head_dim=128, ffn=11008),
+          "tiny": dict(family=E.GPT, vocab=512, hidden=320, heads=4, head_dim=80, ffn=1280)}
 
 
 def run(kind, P, lps, seq, micro, k, mode, model_name="gpt-2.7b"):
