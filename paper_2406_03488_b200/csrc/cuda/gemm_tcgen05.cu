@@ -475,12 +475,18 @@ bool gemm_tc_supported(const GemmArgs& a) {
   return true;
 }
 
+namespace {
+thread_local bool t_single_cta = false;
+}
+void set_gemm_single_cta(bool on) { t_single_cta = on; }
+
 void gemm_tcgen05(const GemmArgs& a, cudaStream_t s) {
   if (!gemm_tc_supported(a)) throw std::invalid_argument("gemm_tcgen05: unsupported operand layout/alignment");
-  static const int force = [] {
+  static const int env_force = [] {
     const char* e = std::getenv("SP_GEMM_CTA");  // tuning: 1 = force the 1-CTA kernel, 2 = force 2-CTA
     return e ? std::atoi(e) : 0;
   }();
+  const int force = t_single_cta ? 1 : env_force;
   // 2-CTA 256x256 tiles once the problem has enough of them to fill the pairs.
   const int64_t tiles2 = ((a.M + 255) / 256) * ((a.N + 255) / 256);
   const bool two = force == 2 || (force != 1 && tiles2 >= num_sms() / 2);

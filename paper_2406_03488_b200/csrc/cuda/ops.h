@@ -47,6 +47,11 @@ void gemm(const GemmArgs& a, cudaStream_t s, int impl = kGemmAuto);
 bool gemm_tc_supported(const GemmArgs& a);
 void gemm_simt(const GemmArgs& a, cudaStream_t s);
 void gemm_tcgen05(const GemmArgs& a, cudaStream_t s);
+// Per host thread: true restricts the tcgen05 GEMM to its 1-CTA kernel (no cta_group::2
+// clusters). Set by engines that share one GPU with other engines' threads (in-process
+// multi-rank): with several engines launching 2-CTA GEMMs concurrently, a pair's
+// cta_group::2 TMEM allocation intermittently never completed (engine.cpp, step()).
+void set_gemm_single_cta(bool on);
 
 // ---------------------------------------------------------------- attention
 // q [n, H*hd] (row stride H*hd), kv [kv_len, 2*H*hd] (K | V per row),

@@ -206,6 +206,7 @@ void Engine::attach_local(std::shared_ptr<LocalHub> hub) {
       max_bytes = std::max(max_bytes, spk::dtype_size(mc_.dt) * static_cast<size_t>(c.elems));
     }
   transport_ = make_local_transport(std::move(hub), rank_, sends, max_bytes);
+  local_transport_ = true;
   comm_ready_setup();
 }
 
@@ -402,6 +403,13 @@ void Engine::step(const int32_t* tokens, bool on_device, sp_step_report* rep) {
   SPK_CUDA(cudaSetDevice(dev_));
   if (world_ > 1 && !transport_)
     throw std::logic_error("multi-rank engine: call sp_engine_comm_init / sp_engine_attach_local first");
+  // Several engines on one GPU (in-process transport, one host thread each): their 2-CTA
+  // GEMMs run concurrently, and a cta_group::2 cluster then intermittently stopped in its
+  // first cluster barrier with one CTA's TMEM allocation never completing (cuda-gdb: the
+  // only kernel left on the GPU; 3 of 4 runs of a 3-stage GPT-2.7B step without side
+  // streams, 0 of 8 with the 1-CTA GEMM). These engines use the 1-CTA GEMM; one engine per
+  // GPU (P = 1, or one process per GPU over NCCL) keeps the 2-CTA kernel.
+  spk::set_gemm_single_cta(local_transport_);
   ++step_no_;
   adam_bc_host_[0] = 1.f - std::pow(mc_.b1, static_cast<float>(step_no_));
   adam_bc_host_[1] = 1.f - std::pow(mc_.b2, static_cast<float>(step_no_));

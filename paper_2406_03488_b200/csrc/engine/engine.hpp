@@ -226,6 +226,7 @@ class Engine {
   // Multi-rank data plane: NCCL communicators from `ids` (one per channel), or an in-process hub.
   void comm_init(const std::vector<std::string>& ids);
   void attach_local(std::shared_ptr<LocalHub> hub);
+  bool local_transport_ = false;  // shares its GPU with other engines' host threads
   int comm_channels() const;
   void step(const int32_t* tokens, bool on_device, sp_step_report* rep);
   // Capture the step (ops + optimizer) once into a CUDA graph and replay it (single-rank engines).

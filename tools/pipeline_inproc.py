@@ -5,9 +5,10 @@ in-process transport exactly as sp_comm_plan lists them (the multi-rank data pla
 engine.cpp; the reference's pipeline edges sim.cpp:20-23 / :31-33).
 
 Per stage it reports what the device holds, measured:
-  * arena_gb_device   -- cudaMemGetInfo delta of creating that stage's engine minus its weights /
-                         optimizer state, i.e. HBM actually reserved for activations (KV slabs,
-                         per-(m,s) records, W records),
+  * activation_gb_device -- cudaMemGetInfo delta of creating that stage's engine minus its
+                         weights / optimizer state: the activation arena (KV slabs, per-(m,s)
+                         records) + the fp32 dK/dV accumulator + per-op workspaces, as allocated,
+  * arena_gb_planned  -- the activation arena alone (what the device allocation holds),
   * peak_activation_gb -- the live high-water of the executed op order (StepReport),
   * bubble_ratio      -- idle / (last_end - first_start) of the stage's stream from per-op CUDA
                          events (sim.cpp:252-254 definition). With P stages time-sharing one GPU
@@ -52,9 +53,9 @@ def run(kind, P, lps, seq, micro, k, mode, model_name="gpt-2.7b"):
     for r in range(P):
         free0, _ = torch.cuda.mem_get_info(0)
         e = E.Engine(cfg, kind, part, model, rank=r, world_size=P, cuda_device=0)
-        e.attach_local(hub)
         torch.cuda.synchronize()
         free1, _ = torch.cuda.mem_get_info(0)
+        e.attach_local(hub)  # (its staging slots are transport memory, not the stage's)
         engines.append(e)
         dev_bytes.append(free0 - free1)
     tok = torch.randint(0, model.vocab, (micro, seq + 1), dtype=torch.int32).numpy()
