@@ -213,9 +213,6 @@ __device__ __forceinline__ float2 ex2x2_sel(bool poly, float2 v) { return poly ?
 #ifndef SPK_DKV_NS
 #define SPK_DKV_NS 3  // hd <= 80 dK/dV: score buffers (the dP^T buffers take the remaining 4 - NS)
 #endif
-#ifndef SPK_DKV_PARITY
-#define SPK_DKV_PARITY 0  // 1 (with SPK_DKV_NS=2): dK/dV softmax warps split by block parity
-#endif
 #ifndef SPK_DQ_NS
 #define SPK_DQ_NS 3  // hd <= 80 dQ: score / dP buffers (3 + 2: -0.5 % bwd at sustained clocks vs 3 + 1)
 #endif
@@ -735,11 +732,11 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
     tc::mbar_init(done, 1);
     for (int i = 0; i < NS; ++i) {
       tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&sm_done[i], SPK_DKV_PARITY && C::KVT ? 8 : 16);  // parity split: 8 warps per block
+      tc::mbar_init(&sm_done[i], 16);
     }
     for (int i = 0; i < ND; ++i) {
       tc::mbar_init(&dp_full[i], 1);
-      tc::mbar_init(&dp_free[i], SPK_DKV_PARITY && C::KVT ? 8 : 16);
+      tc::mbar_init(&dp_free[i], 16);
     }
     for (int i = 0; i < QST; ++i) {
       tc::mbar_init(&q_full[i], 1);
@@ -865,82 +862,6 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
       warp_arrive(kv_full);
     }
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-    if constexpr (SPK_DKV_PARITY && C::KVT) {
-      // Parity split (NS = ND = 2): the warps with (g & 1) == par take the blocks it with
-      // it % 2 == par, each covering 32 query columns (groups 2h, 2h + 1, h = g >> 1) -- two
-      // blocks are in the softmax at once instead of all 16 warps finishing block i before
-      // any starts block i + 1, and S / dP buffer b = d = par.
-      static_assert(NS == 2 && ND == 2, "parity split needs two S and two dP buffers");
-      const int par = g & 1, hh = g >> 1;
-      int st = par % QST;
-      uint32_t ph = 0, ph_st = static_cast<uint32_t>((par / QST) & 1);
-      int cmin = clamp_i32(kpos - p.q_off - ib0 - 64 * par - 32 * hh);
-      int cmin_w = clamp_i32(j0 + quarter * 32 + 31 - p.q_off - ib0 - 64 * par - 32 * hh);
-      int chi = clamp_i32(p.n - ib0 - 64 * par - 32 * hh);
-      for (int it = par; it < niter; it += 2) {
-        tc::mbar_wait(&q_full[st], ph_st);
-        tc::mbar_wait(&s_full[par], ph);
-        tc::tc_fence_after();
-#pragma unroll 1
-        for (int sub = 0; sub < 2; ++sub) {
-          const int gg = 2 * hh + sub;  // 16-query group within the 64-query block
-          const float* nl = sLD + st * 128 + gg * 16;
-          const float* nd = nl + 64;
-          const int cm = cmin - 16 * sub, cmw = cmin_w - 16 * sub, ch = chi - 16 * sub;
-          const int c_lo = cm < 0 ? 0 : (cm > 16 ? 16 : cm);
-          const int c_hi = ch < 0 ? 0 : (ch > 16 ? 16 : ch);
-          const bool full_blk = cmw <= 0 && ch >= 16;
-          uint32_t sv[16], dpv[16];
-          tmem_ld16(tmem + lane_base + par * 64 + gg * 16, sv);
-          if (sub == 0) tc::mbar_wait(&dp_full[par], ph);
-          tc::tc_fence_after();
-          tmem_ld16(tmem + lane_base + C::T_DP + par * 64 + gg * 16, dpv);
-          tc::tmem_ld_wait();
-          if (sub == 1) {
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&dp_free[par]);  // dP^T(it) fully loaded by this warp
-          }
-          uint32_t wp[8], wd[8];
-          auto body = [&](auto masked) {
-#pragma unroll
-            for (int e = 0; e < 16; e += 4) {
-              const float4 l4 = lds_f4(nl + e), d4 = lds_f4(nd + e);
-              const bool poly = bwd_poly_group(2 * (e / 4));
-              float2 p0 = ex2x2_sel(poly, ffma2(u2f2(sv[e], sv[e + 1]), sc2, make_float2(l4.x, l4.y)));
-              float2 p1 = ex2x2_sel(poly, ffma2(u2f2(sv[e + 2], sv[e + 3]), sc2, make_float2(l4.z, l4.w)));
-              if constexpr (decltype(masked)::value) {
-                if (e < c_lo || e >= c_hi) p0.x = 0.f;
-                if (e + 1 < c_lo || e + 1 >= c_hi) p0.y = 0.f;
-                if (e + 2 < c_lo || e + 2 >= c_hi) p1.x = 0.f;
-                if (e + 3 < c_lo || e + 3 >= c_hi) p1.y = 0.f;
-              }
-              const float2 g0 = fmul2(p0, fadd2(u2f2(dpv[e], dpv[e + 1]), make_float2(d4.x, d4.y)));
-              const float2 g1 = fmul2(p1, fadd2(u2f2(dpv[e + 2], dpv[e + 3]), make_float2(d4.z, d4.w)));
-              wp[e / 2] = pack2(p0);
-              wp[e / 2 + 1] = pack2(p1);
-              wd[e / 2] = pack2(g0);
-              wd[e / 2 + 1] = pack2(g1);
-            }
-          };
-          if (full_blk)
-            body(std::false_type{});
-          else
-            body(std::true_type{});
-          tc::tmem_st8(tmem + lane_base + par * 64 + gg * 16, wp);
-          tc::tmem_st8(tmem + lane_base + par * 64 + gg * 16 + 8, wd);
-        }
-        tc::tmem_st_wait();
-        tc::tc_fence_before();
-        warp_arrive(&sm_done[par]);
-        ph ^= 1;
-        st += 2;
-        if (st >= QST) st -= QST, ph_st ^= 1;
-        cmin -= 128;
-        cmin_w -= 128;
-        chi -= 128;
-      }
-    } else {
     // Per-iteration bookkeeping as running counters: ring / buffer indices and mbarrier
     // parities advance without div / mod, and the causal-mask bounds are int32 values
     // stepped by 64 (the 64-bit per-iteration index math was ~2 instructions per score).
@@ -1021,7 +942,6 @@ __global__ void __launch_bounds__(640, 1) attn_bwd_dkv_k(const __grid_constant__
       tc::tc_fence_before();
       warp_arrive(&sm_done[b]);
       if (warp == 4) trace_mark(p, 7, it);
-    }
     }
     tc::mbar_wait(done, 0);
     tc::tc_fence_after();
