@@ -278,11 +278,13 @@ def stage1_budget(W, preset, args, E, pl):
         pl.apply_scenario_override(c, key, str(v))
     part = pl.partition_for(c, args.partition)
 
-    def model(ffn):
-        return E.ModelConfig(family=W["family"], dtype=E.BF16, vocab=V, hidden=h, layers=L, heads=W["H"],
-                             head_dim=W["hd"], ffn=ffn, max_seq=args.seq)
-    live, arena, dkv = E.plan_memory(c, "seq1f1b", part, model(F), stage=1)
-    live_nou, arena_nou, _ = E.plan_memory(c, "seq1f1b", part, model(64), stage=1)
+    def model(flags):
+        m = E.ModelConfig(family=W["family"], dtype=E.BF16, vocab=V, hidden=h, layers=L, heads=W["H"],
+                          head_dim=W["hd"], ffn=F, max_seq=args.seq)
+        m.flags = flags
+        return m
+    live, arena, dkv = E.plan_memory(c, "seq1f1b", part, model(0), stage=1)
+    live_nou, arena_nou, _ = E.plan_memory(c, "seq1f1b", part, model(E.FLAG_RECOMPUTE_MLP), stage=1)
     fup = 2 * F if W["family"] == LLAMA else F
     per_layer = 4 * h * h + (3 if W["family"] == LLAMA else 2) * h * F + 4 * h
     params = (L // P) * per_layer + V * h + (args.seq * h if W["family"] == GPT else 0)
@@ -291,7 +293,7 @@ def stage1_budget(W, preset, args, E, pl):
     ws = 2 * n * (h + 2 * fup + 6 * h) + 4 * n * h + 8 * n * W["H"]
     cap = torch.cuda.mem_get_info(0)[1] if torch.cuda.is_available() else 180e9
     total = weights + dkv + arena + ws
-    total_rc = weights + dkv + arena_nou + ws
+    total_rc = weights + dkv + arena_nou + ws + 2 * n * fup  # + the recomputed-u workspace
     n_tok = sum(part.lengths)
     layer_fl = 2 * n_tok * per_layer  # forward GEMM FLOPs of a layer over the sequence (approx.)
     extra = 2 * n_tok * h * fup / (3 * layer_fl)
@@ -301,7 +303,9 @@ def stage1_budget(W, preset, args, E, pl):
             "live_activation_peak_gb": live / gb, "workspaces_gb": ws / gb, "total_gb": total / gb,
             "device_capacity_gb": cap / gb, "fits": total <= cap,
             "if_oom_plan": None if total <= cap else {
-                "recompute": "MLP up-projection output u recomputed in B (one extra [n,h]x[h,Fup] GEMM per layer)",
+                "recompute": "SP_FLAG_RECOMPUTE_MLP: the MLP up-projection output u is not kept in the (m,s) "
+                             "record and is recomputed in B (one extra [n,h]x[h,Fup] GEMM per layer); engine "
+                             "plan (sp_plan_memory) with the flag",
                 "arena_gb": arena_nou / gb, "live_activation_peak_gb": live_nou / gb, "total_gb": total_rc / gb,
                 "fits": total_rc <= cap, "extra_gemm_flops_frac": extra}}
 
@@ -312,6 +316,7 @@ def config_of(args, micro, seq, k, lengths):
             "partition": list(lengths), "partition_mode": args.partition, "schedule": args.kind,
             "parallelism": f"pp{args.gpus}" if not W["stage_layers"] else f"stage of pp{W['pipeline']} on 1 GPU",
             "layers_on_gpu": W["stage_layers"] or W["L"],
+            "recompute": "mlp-up (SP_FLAG_RECOMPUTE_MLP)" if getattr(args, "recompute_mlp", False) else "none",
             "l2": "inputs larger than L2 (weights + activations >> 126 MB per step)"}
 
 
@@ -331,6 +336,7 @@ def main():
     ap.add_argument("--partition", default="cwp", choices=["cwp", "even"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", type=int, default=1, help="replay the step as a captured CUDA graph (P = 1)")
+    ap.add_argument("--recompute-mlp", action="store_true", help="SP_FLAG_RECOMPUTE_MLP (recompute u in B)")
     args = ap.parse_args()
     W = WORKLOADS[args.workload]
     args.seq = args.seq or W["seq"]
@@ -375,7 +381,7 @@ def main():
         part = pl.make_partition(part_full.lengths, cfg)
     else:
         cfg, part = full, part_full
-    model.flags = E.FLAG_TIMELINE
+    model.flags = E.FLAG_TIMELINE | (E.FLAG_RECOMPUTE_MLP if args.recompute_mlp else 0)
     eng = E.Engine(cfg, args.kind, part, model, rank=rank, world_size=world, cuda_device=local)
     if world > 1:
         n_ids = eng.comm_channels()
@@ -430,9 +436,9 @@ def main():
     e2e_step = max_over_ranks(sum(e2e_ms) / len(e2e_ms))
     loss_last = r.loss
     # ---- untimed probe step: per-class kernel times for the roofline
-    eng.set_flags(E.FLAG_TIMELINE | E.FLAG_KPROBE)
+    eng.set_flags(model.flags | E.FLAG_KPROBE)
     probe = eng.step(tok_ptr, on_device=True)
-    eng.set_flags(E.FLAG_TIMELINE)
+    eng.set_flags(model.flags)
     mem = eng.memory()
 
     tok_per_step = cfg.micro_batches * T

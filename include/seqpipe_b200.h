@@ -277,7 +277,10 @@ enum {
   SP_FLAG_NO_TCGEN05 = 1,   /* bf16 mode: force the SIMT GEMM (debug / A-B testing)   */
   SP_FLAG_NO_TC_ATTN = 2,   /* bf16 mode: force the SIMT attention                    */
   SP_FLAG_TIMELINE = 4,     /* record per-op CUDA events for the measured report      */
-  SP_FLAG_KPROBE = 8        /* CUDA events around every GEMM / attention launch        */
+  SP_FLAG_KPROBE = 8,       /* CUDA events around every GEMM / attention launch        */
+  SP_FLAG_RECOMPUTE_MLP = 16 /* do not keep the MLP up-projection output u in the (m,s) record;
+                                recompute it in B (one extra [n,h]x[h,Fup] GEMM per layer).
+                                Fixed at engine creation (it sizes the activation records). */
 };
 
 typedef struct sp_engine sp_engine;

@@ -76,6 +76,8 @@ Engine::Engine(const seqpipe::ScenarioConfig& cfg, seqpipe::ScheduleKind kind, c
     throw std::invalid_argument("world_size must be 1 (all stages in-process) or pipeline_size");
   if (rank < 0 || rank >= world) throw std::invalid_argument("rank out of range");
   if (mc_.h != mc_.H * mc_.hd) throw std::invalid_argument("hidden must equal heads * head_dim");
+  if ((mc_.flags & SP_FLAG_RECOMPUTE_MLP) && seqpipe::is_zero_bubble(kind))
+    throw std::invalid_argument("SP_FLAG_RECOMPUTE_MLP: the zero-bubble kinds keep the MLP operands for W");
   if (mc_.family == SP_MODEL_GPT && mc_.max_seq < cfg.seq_len) throw std::invalid_argument("max_seq < seq_len");
   if (mc_.dt == DType::kBF16) {  // production mode runs tensor-core kernels only: refuse shapes they cannot take
     if (!(mc_.flags & SP_FLAG_NO_TC_ATTN) && mc_.hd != 64 && mc_.hd != 80 && mc_.hd != 128)

@@ -139,7 +139,10 @@ class Stage {
   void* kv(int m, int layer) const;  // [T, 2h] slab of layer (local index)
   float* dkv(int layer) const { return dkv_ + static_cast<size_t>(layer) * T_ * 2 * mc_.h; }
 
-  void set_flags(int f) { mc_.flags = f; }
+  void set_flags(int f) {  // the record layout flag stays what the stage was built with
+    mc_.flags = (f & ~SP_FLAG_RECOMPUTE_MLP) | (mc_.flags & SP_FLAG_RECOMPUTE_MLP);
+  }
+  bool recompute_mlp() const { return (mc_.flags & SP_FLAG_RECOMPUTE_MLP) != 0; }
   void zero_grads();
   void sync_compute();  // recast the compute-dtype weight copy after a master write
   // AdamW over this stage's parameters; bias corrections {1-b1^t, 1-b2^t} read from device memory
@@ -213,7 +216,7 @@ class Stage {
 
   // workspace
   void *w_a_ = nullptr, *w_big1_ = nullptr, *w_big2_ = nullptr, *w_t1_ = nullptr, *w_t2_ = nullptr, *w_t3_ = nullptr,
-       *w_dqkv_ = nullptr, *w_logits_ = nullptr;
+       *w_dqkv_ = nullptr, *w_logits_ = nullptr, *w_u_ = nullptr;  // w_u_: recomputed u (SP_FLAG_RECOMPUTE_MLP)
   float *w_delta_ = nullptr, *w_dq_ = nullptr, *w_fmean_ = nullptr, *w_frstd_ = nullptr;
   int64_t logits_rows_ = 0;
 };
@@ -246,7 +249,7 @@ class Engine {
   int device() const { return dev_; }
   bool table_from_device() const { return table_from_device_; }
   void set_flags(int f) {
-    mc_.flags = f;
+    mc_.flags = (f & ~SP_FLAG_RECOMPUTE_MLP) | (mc_.flags & SP_FLAG_RECOMPUTE_MLP);
     for (auto& kv : stages_) kv.second->set_flags(f);
   }
 

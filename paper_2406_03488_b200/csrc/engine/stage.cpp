@@ -156,6 +156,7 @@ Stage::Stage(const ModelCfg& m, const seqpipe::ScenarioConfig& cfg, const std::v
   SPK_CUDA(cudaMalloc(&w_a_, esz_ * n * h));
   SPK_CUDA(cudaMalloc(&w_big1_, esz_ * n * mc_.Fup));
   SPK_CUDA(cudaMalloc(&w_big2_, esz_ * n * mc_.Fup));
+  if (recompute_mlp()) SPK_CUDA(cudaMalloc(&w_u_, esz_ * n * mc_.Fup));
   SPK_CUDA(cudaMalloc(&w_t1_, esz_ * n * h));
   SPK_CUDA(cudaMalloc(&w_t2_, esz_ * n * h));
   SPK_CUDA(cudaMalloc(&w_t3_, esz_ * n * h));
@@ -180,7 +181,7 @@ Stage::~Stage() {
   if (s2_) cudaStreamDestroy(s2_);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
-  for (void* p : {(void*)master_, (void*)grad_, (void*)adam_m_, (void*)adam_v_, w_a_, w_big1_, w_big2_, w_t1_, w_t2_,
+  for (void* p : {(void*)master_, (void*)grad_, (void*)adam_m_, (void*)adam_v_, w_a_, w_big1_, w_big2_, w_u_, w_t1_, w_t2_,
                   w_t3_, w_dqkv_, (void*)w_delta_, (void*)w_dq_, (void*)w_fmean_, (void*)w_frstd_, w_logits_,
                   (void*)dkv_, (void*)arena_ptr_})
     if (p) cudaFree(p);
@@ -232,7 +233,7 @@ static int64_t seg_bytes(const ModelCfg& mc, int L_s, int64_t n, size_t esz) {
   int64_t b = 0;
   b += (L_s + 2) * n * h * esz;            // x_in[L_s], x_out, dy_in
   b += 3LL * L_s * n * h * esz;            // q, o, x_mid
-  b += static_cast<int64_t>(L_s) * n * mc.Fup * esz;  // u
+  if (!(mc.flags & SP_FLAG_RECOMPUTE_MLP)) b += static_cast<int64_t>(L_s) * n * mc.Fup * esz;  // u
   b += static_cast<int64_t>(L_s) * n * (4 + mc.H) * 4;  // norm stats + lse
   return b + 256LL * (8 * L_s + 4);        // per-field alignment slack
 }
@@ -418,7 +419,7 @@ void Stage::bind_step() {
         g.q[l] = take(n * h * esz_);
         g.o[l] = take(n * h * esz_);
         g.x_mid[l] = take(n * h * esz_);
-        g.u[l] = take(n * mc_.Fup * esz_);
+        g.u[l] = recompute_mlp() ? nullptr : take(n * mc_.Fup * esz_);
         g.mean1[l] = static_cast<float*>(take(n * 4));
         g.rstd1[l] = static_cast<float*>(take(n * 4));
         g.mean2[l] = static_cast<float*>(take(n * 4));
@@ -587,8 +588,9 @@ void Stage::forward(int m, int s, const int32_t* tokens, double* loss_acc, float
     gemm(g, 2.0 * n * h * h);
     spk::norm_fwd(dt, mc_.rms(), sg.x_mid[l], wm(w.norm2), w_a_, mc_.rms() ? nullptr : sg.mean2[l], sg.rstd2[l], n,
                   mc_.h, mc_.eps, s_);
-    gemm(G(dt, n, mc_.Fup, h, w_a_, h, true, wc(w.w1), h, true, sg.u[l], mc_.Fup, dt), 2.0 * n * mc_.Fup * h);
-    spk::act_fwd(dt, mc_.family, sg.u[l], w_big1_, n, mc_.F, s_);
+    void* u = recompute_mlp() ? w_big2_ : sg.u[l];  // w_big2_ is free in the forward
+    gemm(G(dt, n, mc_.Fup, h, w_a_, h, true, wc(w.w1), h, true, u, mc_.Fup, dt), 2.0 * n * mc_.Fup * h);
+    spk::act_fwd(dt, mc_.family, u, w_big1_, n, mc_.F, s_);
     void* y = (l + 1 < L_s_) ? sg.x_in[l + 1] : sg.x_out;
     g = G(dt, n, h, mc_.F, w_big1_, mc_.F, true, wc(w.w2), mc_.F, true, y, h, dt);
     g.epi = Epi::kAddResid;
@@ -675,9 +677,17 @@ void Stage::backward_impl(int m, int s, void* dx_target, const int32_t* tokens, 
   for (int l = L_s_ - 1; l >= 0; --l) {
     const LayerW& w = lw_[l];
     // ---- MLP: y = x_mid + act(norm2(x_mid) W1^T) W2^T
-    if (!defer_w) {  // recomputed operands of the W2 / W1 weight gradients
+    void* u = sg.u[l];
+    if (recompute_mlp()) {  // u = norm2(x_mid) W1^T again: the same GEMM on the same operands (bit-identical)
+      if (defer_w) throw std::invalid_argument("SP_FLAG_RECOMPUTE_MLP is not supported by the zero-bubble kinds");
       spk::norm_apply(dt, mc_.rms(), sg.x_mid[l], wm(w.norm2), sg.mean2[l], sg.rstd2[l], w_a_, n, mc_.h, s_);
-      spk::act_fwd(dt, mc_.family, sg.u[l], w_big1_, n, F, s_);
+      gemm(G(dt, n, Fu, h, w_a_, h, true, wc(w.w1), h, true, w_u_, Fu, dt), 2.0 * n * Fu * h);
+      u = w_u_;
+      spk::act_fwd(dt, mc_.family, u, w_big1_, n, F, s_);
+      ++launches;
+    } else if (!defer_w) {  // recomputed operands of the W2 / W1 weight gradients
+      spk::norm_apply(dt, mc_.rms(), sg.x_mid[l], wm(w.norm2), sg.mean2[l], sg.rstd2[l], w_a_, n, mc_.h, s_);
+      spk::act_fwd(dt, mc_.family, u, w_big1_, n, F, s_);
     }
     GemmArgs g;
     if (defer_w) {
@@ -689,7 +699,7 @@ void Stage::backward_impl(int m, int s, void* dx_target, const int32_t* tokens, 
     }
     gemm(G(dt, n, F, h, dy, h, true, wc(w.w2), F, false, w_big2_, F, dt), 2.0 * n * h * F);
     join();  // act_bwd overwrites w_big1_
-    spk::act_bwd(dt, mc_.family, sg.u[l], w_big2_, w_big1_, n, F, s_);
+    spk::act_bwd(dt, mc_.family, u, w_big2_, w_big1_, n, F, s_);
     if (defer_w) {
       SPK_CUDA(cudaMemcpyAsync(sg.w_du[l], w_big1_, esz_ * n * Fu, cudaMemcpyDeviceToDevice, s_));
     } else {

@@ -17,7 +17,7 @@ from . import planner as pl
 
 GPT, LLAMA = 0, 1
 F32, BF16 = 0, 1
-FLAG_NO_TCGEN05, FLAG_NO_TC_ATTN, FLAG_TIMELINE, FLAG_KPROBE = 1, 2, 4, 8
+FLAG_NO_TCGEN05, FLAG_NO_TC_ATTN, FLAG_TIMELINE, FLAG_KPROBE, FLAG_RECOMPUTE_MLP = 1, 2, 4, 8, 16
 
 
 @dataclass

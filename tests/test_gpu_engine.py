@@ -366,3 +366,35 @@ def test_fast_loss_drop_is_memorisation_not_a_causal_leak(gpu, family, hd, ffn, 
     eng.close()
     assert losses[-1] < losses[0] - 0.5, losses  # it does fit the batch ...
     assert held_out > math.log(vocab) - 0.1, (held_out, losses)  # ... without predicting unseen tokens
+
+
+@pytest.mark.parametrize("family", [GPT, LLAMA])
+def test_recompute_mlp_is_bit_identical_and_smaller(gpu, family):
+    """SP_FLAG_RECOMPUTE_MLP drops the MLP up-projection output u from every (m,s) record and
+    recomputes it in B with the same GEMM on the same operands: loss and every gradient are
+    bit-identical to the default engine, the activation plan is smaller, and the zero-bubble
+    kinds (which keep the MLP operands for W) refuse the flag."""
+    hd = 128 if family == LLAMA else 80
+    h = 4 * hd
+    ffn = 3 * h if family == LLAMA else 4 * h
+    cfg = pl.ScenarioConfig(pipeline_size=2, micro_batches=4, segments=4, seq_len=2048, layers=4, hidden_dim=h,
+                            param_count=1)
+    tok = tokens_for(4, 2048, 512, seed=21)
+    out = []
+    for flags in (0, E.FLAG_RECOMPUTE_MLP):
+        model = E.ModelConfig(family=family, dtype=E.BF16, vocab=512, hidden=h, layers=4, heads=4, head_dim=hd,
+                              ffn=ffn, max_seq=2048, seed=42)
+        model.flags = flags
+        cfg.param_count = model.param_count()
+        part = pl.cwp_partition(cfg)
+        eng = E.Engine(cfg, "seq1f1b", part, model)
+        rep = eng.step(tok)
+        out.append((rep.loss, rep.peak_activation_bytes, {n: eng.read_grad(n) for n in eng.params()}))
+        eng.close()
+    (l0, m0, g0), (l1, m1, g1) = out
+    assert l0 == l1
+    assert all(np.array_equal(g0[n], g1[n]) for n in g0)
+    assert m1 < m0
+    model.flags = E.FLAG_RECOMPUTE_MLP
+    with pytest.raises(pl.InvalidArgument):
+        E.Engine(cfg, "seqzb1p", pl.cwp_partition(cfg), model)

@@ -30,7 +30,13 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch  # noqa: E402
 
+from paper_2406_03488_b200 import _capi  # noqa: E402
 from paper_2406_03488_b200 import engine as E  # noqa: E402
+
+if "--variant" in sys.argv:  # a tuning build from tools/build_variant.py (investigations only)
+    i = sys.argv.index("--variant")
+    _capi.LIB_PATH = _capi.LIB_PATH.parent / "variants" / f"libseqpipe_b200_{sys.argv[i + 1]}.so"
+    del sys.argv[i:i + 2]
 from paper_2406_03488_b200 import planner as pl  # noqa: E402
 
 MODELS = {"gpt-2.7b": dict(family=E.GPT, vocab=50257, hidden=2560, heads=32, head_dim=80, ffn=10240),
