@@ -256,9 +256,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_k(const __grid_constan
 // kernel (~16 TB/s of L2 reads at 1.4 PFLOP/s). The leader CTA (rank 0) issues
 // the MMAs; both CTAs load their halves with .cta_group::2 TMA completing on
 // the leader's barrier, and both drain their own TMEM rows in the epilogue.
-#ifndef SPK_GEMM_LATE_RELINQUISH
-#define SPK_GEMM_LATE_RELINQUISH 0  // 1: give up the TMEM allocation permit at the end (CUTLASS order)
-#endif
 constexpr int BM2 = 128, BNH = 128, BK2 = 64, ST2 = 6;
 constexpr int A2_BYTES = BM2 * BK2 * 2, B2_BYTES = BNH * BK2 * 2, STAGE2_BYTES = A2_BYTES + B2_BYTES;
 constexpr int SMEM2_BYTES = ST2 * STAGE2_BYTES + 1024 + 256;
@@ -310,9 +307,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc2_k(const __grid_consta
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tmem_slot)),
                  "r"(TMEM_COLS)
                  : "memory");
-#if !SPK_GEMM_LATE_RELINQUISH
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-#endif
   }
   tc::tc_fence_before();
   tc::cluster_sync();
@@ -430,9 +425,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc2_k(const __grid_consta
       if (acc == 0) acc_phase ^= 1;
     }
   }
-#if SPK_GEMM_LATE_RELINQUISH
-  if (warp == 1) asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-#endif
   tc::tc_fence_before();
   tc::cluster_sync();
   tc::tc_fence_after();
