@@ -334,6 +334,8 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int NV, bool RMS>
 __global__ void __launch_bounds__(256) norm_fwd_vec_k(const __nv_bfloat16* __restrict__ x, const float* __restrict__ g,
@@ -385,8 +387,8 @@ __global__ void __launch_bounds__(256) norm_fwd_vec_k(const __nv_bfloat16* __res
 }
 
 // Rows of h >= 2048: G warps per row (G = 2 for h 2048-3072, 4 for h >= 4096), each caching
-// a 1/G slice of the row in registers (NV/G 16-byte vectors per lane). The grid is persistent
-// (3 CTAs per SM striding over rows) and every warp copies its slice of the NEXT row into
+// a 1/G slice of the row and its fp32 gain slice (loaded once) in registers. The grid is
+// persistent (2 CTAs per SM striding over rows) and every warp copies its slice of the NEXT row into
 // shared memory (cp.async, no registers) before reducing the current one: the DRAM latency of
 // row r+1 hides behind the reductions, barrier and stores of row r (one row per warp and no
 // prefetch left the HBM pipe idle between waves: 0.52 of HBM). Each slice computes its own
@@ -397,7 +399,7 @@ struct RowSlice {
   static constexpr int H = 256 * NV, NS = NV / G, RB = 8 / G;  // vectors per lane, rows per CTA
 };
 template <int NV, int G, bool RMS>
-__global__ void __launch_bounds__(256, 3) norm_fwd_rows_k(const __nv_bfloat16* __restrict__ x,
+__global__ void __launch_bounds__(256, 2) norm_fwd_rows_k(const __nv_bfloat16* __restrict__ x,
                                                           const float* __restrict__ g, __nv_bfloat16* __restrict__ y,
                                                           float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                           int64_t n, float eps) {
@@ -417,7 +419,11 @@ __global__ void __launch_bounds__(256, 3) norm_fwd_rows_k(const __nv_bfloat16* _
     cp_async_commit();
   };
   if (row < n) prefetch(row);
-  const float* gs = g + gi * (H / G);
+  // The warp's gain slice is the same for every row it handles: load it once (ncu on the
+  // per-row version: L1/TEX throughput 78 %, half of it the fp32 gain re-read every row).
+  float gk[NS][8];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) ld_f8(g + gi * (H / G) + (k * 32 + lane) * 8, gk[k]);
   for (int par = 0; row < n; row += stride, par ^= 1) {
     Bf8 cur[NS];
     cp_async_wait_all();
@@ -461,11 +467,10 @@ __global__ void __launch_bounds__(256, 3) norm_fwd_rows_k(const __nv_bfloat16* _
     Bf8* yr = reinterpret_cast<Bf8*>(y + row * H) + gi * NS * 32;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      float f[8], gv[8];
+      float f[8];
       bf8_to_f(cur[k], f);
-      ld_f8(gs + (k * 32 + lane) * 8, gv);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) f[e] = (f[e] - mean) * rstd * gv[e];
+      for (int e = 0; e < 8; ++e) f[e] = (f[e] - mean) * rstd * gk[k][e];
       yr[k * 32 + lane] = f_to_bf8(f);
     }
     if (lane == 0 && gi == 0) {
@@ -588,65 +593,64 @@ __global__ void __launch_bounds__(256, 2) norm_bwd_rows_k(const __nv_bfloat16* _
                                                           const float* __restrict__ rstd, const __nv_bfloat16* dres,
                                                           __nv_bfloat16* dx, float* __restrict__ dg, int64_t n) {
   using RS = RowSlice<NV, G>;
-  constexpr int H = RS::H, NS = RS::NS, HS = H / G;
-  // [8 warps][H/G] fp32 dgain partials, then [8 warps][2][NS * 32] Bf8: next row's x / dy slices
-  extern __shared__ float4 sdg4[];
-  float* sdg = reinterpret_cast<float*>(sdg4);
+  constexpr int H = RS::H, NS = RS::NS, HS = H / G, SL = NS * 32;  // SL: 16-byte vectors per slice
+  // per warp: x / dy slices double-buffered + the residual-gradient slice, all filled by
+  // cp.async; reused for the dgain block reduction at the end
+  extern __shared__ float4 sm4[];
+  Bf8* pf = reinterpret_cast<Bf8*>(sm4) + (threadIdx.x >> 5) * 5 * SL;
   __shared__ float2 xch[2][RS::RB][G];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, rb = w / G, gi = w % G;
-  float* my = sdg + w * HS;
-  Bf8* pfx = reinterpret_cast<Bf8*>(sdg + 8 * HS) + w * 2 * NS * 32;
-  Bf8* pfd = pfx + NS * 32;
-  for (int c = lane * 4; c < HS; c += 128) *reinterpret_cast<float4*>(my + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncwarp();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * RS::RB;
   int64_t row = static_cast<int64_t>(blockIdx.x) * RS::RB + rb;
   auto sl = [&](const __nv_bfloat16* base, int64_t r) { return reinterpret_cast<const Bf8*>(base + r * H) + gi * NS * 32; };
-  auto prefetch = [&](int64_t r) {
+  auto prefetch_xdy = [&](int64_t r, int stg) {
     const Bf8 *xr = sl(x, r), *dyr = sl(dy, r);
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      cp_async16(pfx + k * 32 + lane, xr + k * 32 + lane);
-      cp_async16(pfd + k * 32 + lane, dyr + k * 32 + lane);
+      cp_async16(pf + (2 * stg) * SL + k * 32 + lane, xr + k * 32 + lane);
+      cp_async16(pf + (2 * stg + 1) * SL + k * 32 + lane, dyr + k * 32 + lane);
     }
     cp_async_commit();
   };
-  if (row < n) prefetch(row);
-  const float* gs = g + gi * HS;
-  for (int par = 0; row < n; row += stride, par ^= 1) {
-    Bf8 xv[NS], dv[NS], rv[NS];
-    if (dres) {  // residual gradient: its latency hides behind the two reductions
+  // gain slice and dgain partials stay in registers across the warp's rows (per-row re-reads
+  // of the fp32 gain and a shared-memory read-modify-write of the partials kept the per-row
+  // kernel L1-bound)
+  float gk[NS][8], dga[NS][8];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    ld_f8(g + gi * HS + (k * 32 + lane) * 8, gk[k]);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) dga[k][e] = 0.f;
+  }
+  if (row < n) prefetch_xdy(row, 0);
+  for (int par = 0, stg = 0; row < n; row += stride, par ^= 1, stg ^= 1) {
+    const bool more = row + stride < n;
+    if (dres) {  // group: residual gradient of this row
       const Bf8* rr = sl(dres, row);
 #pragma unroll
-      for (int k = 0; k < NS; ++k) rv[k] = rr[k * 32 + lane];
+      for (int k = 0; k < NS; ++k) cp_async16(pf + 4 * SL + k * 32 + lane, rr + k * 32 + lane);
     }
-    cp_async_wait_all();
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      xv[k] = pfx[k * 32 + lane];
-      dv[k] = pfd[k * 32 + lane];
-    }
-    if (row + stride < n) prefetch(row + stride);
-    const float mu = RMS ? 0.f : mean[row], rs = rstd[row];
+    cp_async_commit();
+    if (more) prefetch_xdy(row + stride, stg ^ 1);  // group: next row's x / dy
+    if (more)
+      cp_async_wait<2>();  // this row's x / dy landed (issued one iteration ago)
+    else
+      cp_async_wait<1>();
+    const Bf8 *xs = pf + (2 * stg) * SL, *ds = xs + SL, *rs = pf + 4 * SL;
+    const float mu = RMS ? 0.f : mean[row], rsd = rstd[row];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      float f[8], d[8], gv[8];
-      bf8_to_f(xv[k], f);
-      bf8_to_f(dv[k], d);
-      ld_f8(gs + (k * 32 + lane) * 8, gv);
-      float* acc = my + (k * 32 + lane) * 8;
-      float4 a0 = *reinterpret_cast<float4*>(acc), a1 = *reinterpret_cast<float4*>(acc + 4);
-      float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      float f[8], d[8];
+      bf8_to_f(xs[k * 32 + lane], f);
+      bf8_to_f(ds[k * 32 + lane], d);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float xh = (f[e] - mu) * rs, dxh = d[e] * gv[e];
+        const float xh = (f[e] - mu) * rsd, dxh = d[e] * gk[k][e];
         s1 += dxh;
         s2 += dxh * xh;
-        av[e] += d[e] * xh;
+        dga[k][e] += d[e] * xh;
       }
-      *reinterpret_cast<float4*>(acc) = make_float4(av[0], av[1], av[2], av[3]);
-      *reinterpret_cast<float4*>(acc + 4) = make_float4(av[4], av[5], av[6], av[7]);
     }
     s1 = RMS ? 0.f : warp_sum(s1);
     s2 = warp_sum(s2);
@@ -659,21 +663,33 @@ __global__ void __launch_bounds__(256, 2) norm_bwd_rows_k(const __nv_bfloat16* _
       t2 += xch[par][rb][q].y;
     }
     const float m1 = RMS ? 0.f : t1 / H, m2 = t2 / H;
+    if (more)
+      cp_async_wait<1>();  // the residual gradient landed
+    else
+      cp_async_wait<0>();
     Bf8* dxr = reinterpret_cast<Bf8*>(dx + row * H) + gi * NS * 32;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      float f[8], d[8], gv[8], r[8];
-      bf8_to_f(xv[k], f);
-      bf8_to_f(dv[k], d);
-      ld_f8(gs + (k * 32 + lane) * 8, gv);
-      if (dres) bf8_to_f(rv[k], r);
+      float f[8], d[8], r[8];
+      bf8_to_f(xs[k * 32 + lane], f);
+      bf8_to_f(ds[k * 32 + lane], d);
+      if (dres) bf8_to_f(rs[k * 32 + lane], r);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float xh = (f[e] - mu) * rs;
-        f[e] = rs * (d[e] * gv[e] - m1 - xh * m2) + (dres ? r[e] : 0.f);
+        const float xh = (f[e] - mu) * rsd;
+        f[e] = rsd * (d[e] * gk[k][e] - m1 - xh * m2) + (dres ? r[e] : 0.f);
       }
       dxr[k * 32 + lane] = f_to_bf8(f);
     }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  float* sdg = reinterpret_cast<float*>(sm4);  // [8 warps][H/G]
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    float* dst = sdg + w * HS + (k * 32 + lane) * 8;
+    *reinterpret_cast<float4*>(dst) = make_float4(dga[k][0], dga[k][1], dga[k][2], dga[k][3]);
+    *reinterpret_cast<float4*>(dst + 4) = make_float4(dga[k][4], dga[k][5], dga[k][6], dga[k][7]);
   }
   __syncthreads();
   for (int c = threadIdx.x; c < H; c += 256) {
@@ -876,7 +892,7 @@ void norm_fwd(DType t, bool rms, const void* x, const float* g, void* y, float* 
         if constexpr (NV >= 8 && NV % 2 == 0) {
           constexpr int G = NV >= 16 ? 4 : 2;
           const int64_t blocks = (n + 8 / G - 1) / (8 / G);
-          const unsigned grid = static_cast<unsigned>(std::min<int64_t>(blocks, 3 * num_sms()));
+          const unsigned grid = static_cast<unsigned>(std::min<int64_t>(blocks, 2 * num_sms()));
           const size_t pf = 8 * (NV / G) * 32 * 16;  // next-row slices, [8 warps][NS * 32] x 16 B
           if (rms)
             norm_fwd_rows_k<NV, G, true><<<grid, 256, pf, s>>>(xb, g, yb, mean, rstd, n, eps);
@@ -942,7 +958,7 @@ void norm_bwd(DType t, bool rms, const void* dy, const void* x, const float* g, 
         };
         if constexpr (NV >= 8 && NV % 2 == 0) {  // G warps per row, persistent, next row prefetched
           constexpr int G = NV >= 16 ? 4 : 2;
-          const size_t sm2 = sizeof(float) * 8 * (256 * NV / G) + 8 * 2 * (NV / G) * 32 * 16;
+          const size_t sm2 = std::max<size_t>(8 * 5 * (NV / G) * 32 * 16, sizeof(float) * 8 * (256 * NV / G));
           const int64_t b2 = (n + 8 / G - 1) / (8 / G);
           const unsigned grid2 = static_cast<unsigned>(std::min<int64_t>(b2, 2 * num_sms()));
           auto launch2 = [&](auto kern) {

