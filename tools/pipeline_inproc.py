@@ -126,7 +126,11 @@ def main():
         for pt in a.sweep.split(","):
             T, k, P = (int(v) for v in pt.split(":"))
             kind = "seq1f1b" if k > 1 else "1f1b"
-            r = run(kind, P, a.layers_per_stage, T, 2 * P, k, a.partition, a.model)
+            try:
+                r = run(kind, P, a.layers_per_stage, T, 2 * P, k, a.partition, a.model)
+            except Exception as ex:  # noqa: BLE001 -- e.g. a point whose P engines do not fit one GPU
+                r = {"model": a.model, "kind": kind, "P": P, "seq": T, "segments": k, "error": str(ex)[:200]}
+                torch.cuda.empty_cache()
             print(json.dumps(r), flush=True)
         return
     res = {}
