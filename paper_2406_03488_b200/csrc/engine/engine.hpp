@@ -229,7 +229,6 @@ class Engine {
   // Multi-rank data plane: NCCL communicators from `ids` (one per channel), or an in-process hub.
   void comm_init(const std::vector<std::string>& ids);
   void attach_local(std::shared_ptr<LocalHub> hub);
-  bool local_transport_ = false;  // shares its GPU with other engines' host threads
   int comm_channels() const;
   void step(const int32_t* tokens, bool on_device, sp_step_report* rep);
   // Capture the step (ops + optimizer) once into a CUDA graph and replay it (single-rank engines).
@@ -254,6 +253,7 @@ class Engine {
   }
 
  private:
+  bool local_transport_ = false;  // attached to the in-process hub: shares its GPU with other engines' threads
   void enqueue_ops();  // every op of this process's order (+ transfers), on the engine streams
   void exec_op(const seqpipe::Task& t, int order_index, int device_pos);
   // Receive side of one channel: R staging slots so receives are posted ahead of the op that
