@@ -337,6 +337,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", type=int, default=1, help="replay the step as a captured CUDA graph (P = 1)")
     ap.add_argument("--recompute-mlp", action="store_true", help="SP_FLAG_RECOMPUTE_MLP (recompute u in B)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
+                    help="N > 1: NCCL P2P, or the peer-memory transport (CUDA IPC rings over NVLink)")
     args = ap.parse_args()
     W = WORKLOADS[args.workload]
     args.seq = args.seq or W["seq"]
@@ -383,7 +385,11 @@ def main():
         cfg, part = full, part_full
     model.flags = E.FLAG_TIMELINE | (E.FLAG_RECOMPUTE_MLP if args.recompute_mlp else 0)
     eng = E.Engine(cfg, args.kind, part, model, rank=rank, world_size=world, cuda_device=local)
-    if world > 1:
+    if world > 1 and args.transport == "ipc":
+        blobs = [None] * world
+        dist.all_gather_object(blobs, eng.ipc_export())
+        eng.ipc_connect(blobs)
+    elif world > 1:
         n_ids = eng.comm_channels()
         ids = [E.nccl_unique_id() for _ in range(n_ids)] if rank == 0 else [None] * n_ids
         dist.broadcast_object_list(ids, src=0)

@@ -332,6 +332,14 @@ typedef struct sp_local_hub sp_local_hub;
 int sp_engine_comm_channels(sp_engine* eng, int32_t* n);
 int sp_nccl_unique_id(uint8_t* out, size_t len);
 int sp_engine_comm_init(sp_engine* eng, const uint8_t* const* ids, int32_t n_ids);
+/* Peer-memory data plane instead of NCCL (one process per GPU, CUDA IPC): every rank calls
+ * sp_engine_ipc_export (size query with out == NULL, then the copy; it allocates the rank's
+ * receive rings and flag words once), the blobs travel over any side channel, then every rank
+ * calls sp_engine_ipc_connect with all of them in rank order. A message is one device-to-device
+ * copy into the receiver's ring plus a release / acquire flag pair; a transfer that never pairs
+ * up traps the CUDA context after the engine's watchdog time. */
+int sp_engine_ipc_export(sp_engine* eng, uint8_t* out, size_t* len);
+int sp_engine_ipc_connect(sp_engine* eng, const uint8_t* const* blobs, const size_t* lens, int32_t n);
 int sp_local_hub_create(int32_t world_size, double watchdog_seconds, sp_local_hub** out);
 int sp_local_hub_destroy(sp_local_hub* hub);
 int sp_engine_attach_local(sp_engine* eng, sp_local_hub* hub);

@@ -126,6 +126,8 @@ _SIGS = {
     "sp_plan_memory": (C.c_int, [P(Scenario), C.c_int32, P(C.c_int64), P(Model), C.c_int32, P(C.c_double),
                                  P(C.c_double), P(C.c_double)]),
     "sp_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_size_t]),
+    "sp_engine_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, P(C.c_size_t)]),
+    "sp_engine_ipc_connect": (C.c_int, [C.c_void_p, P(C.c_void_p), P(C.c_size_t), C.c_int32]),
     "sp_engine_comm_init": (C.c_int, [C.c_void_p, P(C.c_char_p), C.c_int32]),
     "sp_engine_comm_channels": (C.c_int, [C.c_void_p, P(C.c_int32)]),
     "sp_local_hub_create": (C.c_int, [C.c_int32, C.c_double, P(C.c_void_p)]),

@@ -150,6 +150,30 @@ int sp_engine_comm_init(sp_engine* eng, const uint8_t* const* ids, int32_t n_ids
   });
 }
 
+int sp_engine_ipc_export(sp_engine* eng, uint8_t* out, size_t* len) {
+  return eguard([&] {
+    if (!len) throw std::invalid_argument("null length");
+    const std::string b = E(eng).ipc_export();
+    if (out) {
+      if (*len < b.size()) {
+        *len = b.size();
+        throw spc::SpStatusError(SP_ERR_BUFFER_TOO_SMALL, "ipc blob needs " + std::to_string(b.size()) + " bytes");
+      }
+      std::memcpy(out, b.data(), b.size());
+    }
+    *len = b.size();
+  });
+}
+
+int sp_engine_ipc_connect(sp_engine* eng, const uint8_t* const* blobs, const size_t* lens, int32_t n) {
+  return eguard([&] {
+    if (n < 0 || (n > 0 && (!blobs || !lens))) throw std::invalid_argument("null blobs");
+    std::vector<std::string> v;
+    for (int32_t i = 0; i < n; ++i) v.emplace_back(reinterpret_cast<const char*>(blobs[i]), lens[i]);
+    E(eng).ipc_connect(v);
+  });
+}
+
 int sp_engine_comm_channels(sp_engine* eng, int32_t* n) {
   return eguard([&] { *n = E(eng).comm_channels(); });
 }

@@ -198,6 +198,40 @@ void Engine::comm_init(const std::vector<std::string>& ids) {
   comm_ready_setup();
 }
 
+std::string Engine::ipc_export() {
+  if (world_ == 1) throw std::logic_error("ipc_export: world size 1 has no transfers");
+  if (ipc_) return ipc_blob_;  // exported already (a size query, then the copy)
+  SPK_CUDA(cudaSetDevice(dev_));
+  std::vector<int> recv_channels;
+  size_t max_bytes = 0;
+  for (const sp_comm_op& c : plan_) {
+    max_bytes = std::max(max_bytes, spk::dtype_size(mc_.dt) * static_cast<size_t>(c.elems));
+    if (c.dir == SP_COMM_RECV && std::find(recv_channels.begin(), recv_channels.end(), c.channel) == recv_channels.end())
+      recv_channels.push_back(c.channel);
+  }
+  // every rank must size its rings alike: the largest message of any rank is a segment's [n, h]
+  int64_t nmax = 0;
+  for (int64_t n : len_) nmax = std::max(nmax, n);
+  max_bytes = std::max(max_bytes, spk::dtype_size(mc_.dt) * static_cast<size_t>(nmax) * static_cast<size_t>(mc_.h));
+  auto t = make_ipc_transport(rank_, comm_channels(), recv_channels, max_bytes, watchdog_s_);
+  ipc_blob_ = t->export_blob();
+  ipc_ = t.get();
+  transport_ = std::move(t);
+  return ipc_blob_;
+}
+
+void Engine::ipc_connect(const std::vector<std::string>& blobs) {
+  if (!ipc_) throw std::logic_error("ipc_connect: call ipc_export first");
+  if (static_cast<int>(blobs.size()) != world_) throw std::invalid_argument("ipc_connect expects one blob per rank");
+  SPK_CUDA(cudaSetDevice(dev_));
+  std::vector<int> send_peer(static_cast<size_t>(comm_channels()), -1), recv_peer(send_peer);
+  for (const sp_comm_op& c : plan_)
+    (c.dir == SP_COMM_SEND ? send_peer : recv_peer)[static_cast<size_t>(c.channel)] = c.peer;
+  ipc_->connect(blobs, send_peer, recv_peer);
+  ipc_ = nullptr;
+  comm_ready_setup();
+}
+
 void Engine::attach_local(std::shared_ptr<LocalHub> hub) {
   if (world_ == 1) return;
   SPK_CUDA(cudaSetDevice(dev_));

@@ -229,6 +229,10 @@ class Engine {
   // Multi-rank data plane: NCCL communicators from `ids` (one per channel), or an in-process hub.
   void comm_init(const std::vector<std::string>& ids);
   void attach_local(std::shared_ptr<LocalHub> hub);
+  // Peer-memory (CUDA IPC) data plane: export this rank's rings / flags, then connect with
+  // every rank's blob (rank order).
+  std::string ipc_export();
+  void ipc_connect(const std::vector<std::string>& blobs);
   int comm_channels() const;
   void step(const int32_t* tokens, bool on_device, sp_step_report* rep);
   // Capture the step (ops + optimizer) once into a CUDA graph and replay it (single-rank engines).
@@ -254,6 +258,8 @@ class Engine {
 
  private:
   bool local_transport_ = false;  // attached to the in-process hub: shares its GPU with other engines' threads
+  IpcExporter* ipc_ = nullptr;    // transport_ when it is the IPC transport (between export and connect)
+  std::string ipc_blob_;
   void enqueue_ops();  // every op of this process's order (+ transfers), on the engine streams
   void exec_op(const seqpipe::Task& t, int order_index, int device_pos);
   // Receive side of one channel: R staging slots so receives are posted ahead of the op that

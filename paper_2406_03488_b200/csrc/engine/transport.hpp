@@ -8,9 +8,11 @@
 // of a channel are FIFO-ordered identically on both sides (checked when the
 // engine is built, comm_plan_check()).
 //
-// Two transports implement the same stream-ordered send / recv:
+// Three transports implement the same stream-ordered send / recv:
 //   * NcclTransport  -- production: one NCCL communicator per channel, ncclSend /
 //     ncclRecv over NVLink between processes (one process per GPU).
+//   * IpcTransport   -- one process per GPU, copies straight into the receiver's memory
+//     over CUDA-IPC-mapped rings with flag words (transport_ipc.cu);
 //   * LocalTransport -- several engines in one process (one host thread each, on
 //     one or more GPUs): the sender copies the message into a hub-owned staging
 //     buffer on its stream and records an event; the receiver's stream waits on
@@ -52,6 +54,20 @@ class Transport {
 };
 
 std::unique_ptr<Transport> make_nccl_transport(int world, int rank, const std::vector<std::string>& ids);
+
+// Peer-memory transport (transport_ipc.cu): one process per GPU, the receive rings and flag
+// words of every rank exported with CUDA IPC and mapped by its neighbours. Two-phase set-up:
+// every rank exports a blob, the blobs travel over any side channel (rank order), then every
+// rank connects with all of them.
+class IpcExporter : public Transport {
+ public:
+  virtual std::string export_blob() const = 0;
+  // send_peer[c] / recv_peer[c]: peer rank of this rank's send / receive channel c, or -1
+  virtual void connect(const std::vector<std::string>& blobs, const std::vector<int>& send_peer,
+                       const std::vector<int>& recv_peer) = 0;
+};
+std::unique_ptr<IpcExporter> make_ipc_transport(int rank, int channels, const std::vector<int>& recv_channels,
+                                                size_t slot_bytes, double timeout_s);
 
 struct LocalHub;
 std::shared_ptr<LocalHub> make_local_hub(int world, double watchdog_seconds);

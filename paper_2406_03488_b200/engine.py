@@ -99,6 +99,21 @@ class Engine:
         arr = (C.c_char_p * len(ids))(*ids)
         _check(_capi.lib().sp_engine_comm_init(self._h, arr, len(ids)))
 
+    def ipc_export(self) -> bytes:
+        """Peer-memory data plane (one process per GPU, CUDA IPC), phase 1: this rank's blob."""
+        n = C.c_size_t(0)
+        _check(_capi.lib().sp_engine_ipc_export(self._h, None, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _check(_capi.lib().sp_engine_ipc_export(self._h, buf, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def ipc_connect(self, blobs: list):
+        """Phase 2: every rank's blob, in rank order (exchanged over any side channel)."""
+        keep = [C.create_string_buffer(b, len(b)) for b in blobs]
+        ptrs = (C.c_void_p * len(blobs))(*[C.cast(k, C.c_void_p) for k in keep])
+        lens = (C.c_size_t * len(blobs))(*[len(b) for b in blobs])
+        _check(_capi.lib().sp_engine_ipc_connect(self._h, ptrs, lens, len(blobs)))
+
     def attach_local(self, hub: "LocalHub"):
         """In-process data plane: several engines of one process (one host thread each)."""
         self._hub = hub  # keep the hub alive as long as the engine
