@@ -274,4 +274,6 @@ void attn_bwd_simt(DType t, const void* q, const void* kv, const void* o, const 
   SPK_LAUNCH_CHECK();
 }
 
+const void* module_anchor_attention_simt() { return reinterpret_cast<const void*>(&attn_fwd_simt_k<float>); }
+
 }  // namespace spk

@@ -1485,4 +1485,6 @@ void attn_bwd_tc(bool dkv_overwrite, const void* q, const void* kv, const void* 
   }
 }
 
+const void* module_anchor_attention_tc() { return reinterpret_cast<const void*>(&attn_fwd_tc_k<64>); }
+
 }  // namespace spk

@@ -111,4 +111,6 @@ void gemm_simt(const GemmArgs& a, cudaStream_t s) {
   SPK_LAUNCH_CHECK();
 }
 
+const void* module_anchor_gemm_simt() { return reinterpret_cast<const void*>(&gemm_simt_k<float, float>); }
+
 }  // namespace spk

@@ -555,4 +555,6 @@ void gemm(const GemmArgs& a, cudaStream_t s, int impl) {
   gemm_tcgen05(a, s);
 }
 
+const void* module_anchor_gemm_tcgen05() { return reinterpret_cast<const void*>(&gemm_tc_k<float>); }
+
 }  // namespace spk

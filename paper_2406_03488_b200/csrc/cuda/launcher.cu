@@ -7,12 +7,17 @@
 // round-to-nearest intrinsics so no FMA contraction can change a bit.
 // Op tables: closed form of the gpipe / 1f1b / seq1f1b device orders
 // (schedule.cpp:68-126), identical to seqpipe::op_at on the host.
+#include <cuda.h>
+
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include "capi/capi_common.hpp"
 #include "cuda/common.cuh"
 #include "seqpipe/partition.hpp"
 #include "seqpipe/schedule.hpp"
+#include "cuda/ops.h"
 #include "seqpipe_b200.h"
 
 namespace spk {
@@ -221,6 +226,59 @@ std::vector<sp_task> device_op_table(const seqpipe::ScenarioConfig& cfg, seqpipe
   SPK_CUDA(e1);
   SPK_CUDA(e2);
   return out;
+}
+
+namespace {
+
+template <typename F>
+F driver_fn(const char* name) {
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    throw CudaError(std::string("driver entry point unavailable: ") + name);
+  return reinterpret_cast<F>(f);
+}
+
+void preload_module_of(const void* anchor) {
+  using GetLibrary = CUresult (*)(CUlibrary*, CUkernel);
+  using KernelCount = CUresult (*)(unsigned int*, CUlibrary);
+  using Enumerate = CUresult (*)(CUkernel*, unsigned int, CUlibrary);
+  using GetFunction = CUresult (*)(CUfunction*, CUkernel);
+  static const auto get_library = driver_fn<GetLibrary>("cuKernelGetLibrary");
+  static const auto kernel_count = driver_fn<KernelCount>("cuLibraryGetKernelCount");
+  static const auto enumerate = driver_fn<Enumerate>("cuLibraryEnumerateKernels");
+  static const auto get_function = driver_fn<GetFunction>("cuKernelGetFunction");
+  cudaKernel_t k = nullptr;
+  SPK_CUDA(cudaGetKernel(&k, anchor));
+  CUlibrary lib = nullptr;
+  unsigned int n = 0;
+  auto ok = [](CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) throw CudaError(std::string(what) + " failed: " + std::to_string(static_cast<int>(r)));
+  };
+  ok(get_library(&lib, reinterpret_cast<CUkernel>(k)), "cuKernelGetLibrary");
+  ok(kernel_count(&n, lib), "cuLibraryGetKernelCount");
+  std::vector<CUkernel> ks(n);
+  ok(enumerate(ks.data(), n, lib), "cuLibraryEnumerateKernels");
+  for (CUkernel kk : ks) {
+    CUfunction f = nullptr;
+    ok(get_function(&f, kk), "cuKernelGetFunction");  // loads it into the current context
+  }
+}
+
+}  // namespace
+
+void preload_kernels() {
+  static std::mutex mu;
+  static std::set<int> done;  // devices whose context holds every kernel
+  int dev = 0;
+  SPK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(dev)) return;
+  for (const void* a : {module_anchor_attention_simt(), module_anchor_attention_tc(), module_anchor_elementwise(),
+                        module_anchor_gemm_simt(), module_anchor_gemm_tcgen05(),
+                        reinterpret_cast<const void*>(&cwp_kernel)})
+    preload_module_of(a);
+  done.insert(dev);
 }
 
 }  // namespace spk

@@ -101,4 +101,19 @@ void fill_const(float* p, int64_t n, float v, cudaStream_t s);
 void adamw(float* p, const float* g, float* m, float* v, void* pc, DType t, int64_t n, float lr, float b1, float b2,
            float eps, float wd, const float* bc, cudaStream_t s);
 
+// ---------------------------------------------------------------- module loading
+// Loads every kernel of this library into the current device's context now. Under lazy
+// module loading (CUDA_MODULE_LOADING=LAZY, the CUDA 12 default) a kernel is loaded at its
+// first launch and the load waits for the context to go idle; a rank whose streams are
+// parked on a peer's transfer (stream wait / NCCL receive) then blocks its host thread in
+// the launch, and two ranks doing so wait on each other forever. Multi-rank engines call
+// this before their first step. One kernel of each translation unit (module_anchor_*)
+// names its module; the rest are enumerated from it.
+void preload_kernels();
+const void* module_anchor_attention_simt();
+const void* module_anchor_attention_tc();
+const void* module_anchor_elementwise();
+const void* module_anchor_gemm_simt();
+const void* module_anchor_gemm_tcgen05();
+
 }  // namespace spk

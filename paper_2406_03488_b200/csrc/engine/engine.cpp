@@ -140,6 +140,7 @@ Engine::Engine(const seqpipe::ScenarioConfig& cfg, seqpipe::ScheduleKind kind, c
   SPK_CUDA(cudaMalloc(&loss_dev_, sizeof(double)));
   SPK_CUDA(cudaMalloc(&adam_bc_dev_, 2 * sizeof(float)));
   SPK_CUDA(cudaMallocHost(&adam_bc_host_, 2 * sizeof(float)));
+  SPK_CUDA(cudaMallocHost(&loss_host_, sizeof(double)));
   const size_t nops = replay_.size();
   ev_start_.resize(nops);
   ev_end_.resize(nops);
@@ -182,6 +183,7 @@ Engine::~Engine() {
   if (loss_dev_) cudaFree(loss_dev_);
   if (adam_bc_dev_) cudaFree(adam_bc_dev_);
   if (adam_bc_host_) cudaFreeHost(adam_bc_host_);
+  if (loss_host_) cudaFreeHost(loss_host_);
   if (s_) cudaStreamDestroy(s_);
   (void)cudaGetLastError();  // teardown errors must not surface in the next API call of this thread
 }
@@ -248,6 +250,7 @@ void Engine::attach_local(std::shared_ptr<LocalHub> hub) {
 
 // Streams, staging slots and events of this rank's channels.
 void Engine::comm_ready_setup() {
+  spk::preload_kernels();  // no lazy kernel load may stall a launch behind a parked receive (ops.h)
   const int64_t nmax = *std::max_element(len_.begin(), len_.end());
   const size_t max_bytes = spk::dtype_size(mc_.dt) * nmax * mc_.h;
   for (const sp_comm_op& c : plan_) {
@@ -494,8 +497,8 @@ void Engine::step(const int32_t* tokens, bool on_device, sp_step_report* rep) {
   } else {
     enqueue_ops();
   }
-  double loss_h = 0;
-  SPK_CUDA(cudaMemcpyAsync(&loss_h, loss_dev_, sizeof(double), cudaMemcpyDeviceToHost, s_));
+  // pinned: a pageable read-back would block this thread until the step ends, before the watchdog
+  SPK_CUDA(cudaMemcpyAsync(loss_host_, loss_dev_, sizeof(double), cudaMemcpyDeviceToHost, s_));
   SPK_CUDA(cudaEventRecord(ev_step1_, s_));
   if (world_ > 1 && watchdog_s_ > 0) {  // a transfer that never pairs up must not hang the process
     const auto t0 = std::chrono::steady_clock::now();
@@ -537,7 +540,7 @@ void Engine::step(const int32_t* tokens, bool on_device, sp_step_report* rep) {
     rep->last_end_ms = last;
     const double window = last - first;
     rep->bubble_ratio = window > 0 ? std::max(0.0, (window - busy) / window) : 0.0;
-    rep->loss = loss_h / (static_cast<double>(cfg_.micro_batches) * cfg_.seq_len);
+    rep->loss = *loss_host_ / (static_cast<double>(cfg_.micro_batches) * cfg_.seq_len);
     double peak = 0, arena = 0, wbytes = 0, flops = 0;
     int64_t launches = 0;
     for (auto& [v, st] : stages_) {

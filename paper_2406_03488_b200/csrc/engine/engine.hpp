@@ -297,6 +297,7 @@ class Engine {
   double* loss_dev_ = nullptr;
   float* adam_bc_dev_ = nullptr;   // {1 - b1^t, 1 - b2^t} of the current step (device)
   float* adam_bc_host_ = nullptr;  // pinned staging for it
+  double* loss_host_ = nullptr;    // pinned loss read-back
   int step_no_ = 0;
   std::vector<seqpipe::Task> op_log_;
   std::vector<cudaEvent_t> ev_start_, ev_end_;

@@ -11,9 +11,11 @@
 //   receiver: wait ready[c] >= seq + 1            (ld.acquire.sys)
 //             copy ring slot -> buf
 //             consumed[c] := seq + 1              (the sender's flag word)
-// All of it is enqueued on the caller's stream (the waits are one-thread spin kernels with a
-// global-timer timeout that traps, so a transfer that never pairs up fails the context instead
-// of hanging it). Counters grow monotonically across steps.
+// All of it is enqueued on the caller's stream as stream memory operations (cuStreamWaitValue64 /
+// cuStreamWriteValue64: the stream front end waits, no SM spins); a transfer that never pairs up
+// is caught by the engine's step watchdog, which releases the waits (abort) and raises
+// DeadlockError. Counters grow monotonically across steps.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -30,22 +32,42 @@ namespace {
 
 constexpr int kIpcSlots = 2;
 
-__global__ void ipc_wait_k(const unsigned long long* flag, unsigned long long target, unsigned long long timeout_ns) {
-  unsigned long long t0, t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  for (;;) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
-    if (v >= target) return;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > timeout_ns) __trap();  // the peer never sent / consumed: fail the context
-    __nanosleep(2000);
-  }
+// Stream memory operations (driver API, resolved once): the stream itself waits on / writes the
+// flag word -- no kernel occupies an SM while waiting, so ranks that time-share one GPU (separate
+// contexts) and ranks on different GPUs behave the same. The write is ordered after the
+// stream's prior work (the ring copy) by the default memory barrier.
+using WaitValue64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+using WriteValue64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+struct StreamMemOps {
+  WaitValue64 wait = nullptr;
+  WriteValue64 write = nullptr;
+};
+const StreamMemOps& mem_ops() {
+  static const StreamMemOps ops = [] {
+    StreamMemOps o;
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      o.wait = reinterpret_cast<WaitValue64>(f);
+    f = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      o.write = reinterpret_cast<WriteValue64>(f);
+    if (!o.wait || !o.write) throw std::runtime_error("ipc transport: stream memory operations unavailable");
+    return o;
+  }();
+  return ops;
 }
-
-__global__ void ipc_signal_k(unsigned long long* flag, unsigned long long value) {
-  __threadfence_system();
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+void wait_geq(cudaStream_t s, const unsigned long long* flag, unsigned long long v) {
+  const CUresult r = mem_ops().wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), v,
+                                    CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) throw ::spk::CudaError("cuStreamWaitValue64 failed: " + std::to_string(static_cast<int>(r)));
+}
+void write_value(cudaStream_t s, unsigned long long* flag, unsigned long long v) {
+  const CUresult r = mem_ops().write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), v,
+                                     CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) throw ::spk::CudaError("cuStreamWriteValue64 failed: " + std::to_string(static_cast<int>(r)));
 }
 
 struct BlobHeader {
@@ -61,7 +83,7 @@ struct BlobChannel {
 class IpcTransport final : public IpcExporter {
  public:
   IpcTransport(int rank, int channels, const std::vector<int>& recv_channels, size_t slot_bytes, double timeout_s)
-      : rank_(rank), C_(channels), slot_bytes_(slot_bytes), timeout_ns_(static_cast<unsigned long long>(timeout_s * 1e9)) {
+      : rank_(rank), C_(channels), slot_bytes_(slot_bytes) {
     SPK_CUDA(cudaMalloc(&flags_, sizeof(unsigned long long) * 2 * C_));
     SPK_CUDA(cudaMemset(flags_, 0, sizeof(unsigned long long) * 2 * C_));
     for (int c : recv_channels) {
@@ -152,28 +174,31 @@ class IpcTransport final : public IpcExporter {
     uint8_t* ring = peer_ring_[static_cast<size_t>(channel)];
     if (!ring || send_peer_.at(channel) != peer) throw std::logic_error("ipc: send on an unconnected channel");
     const unsigned long long seq = send_seq_[static_cast<size_t>(channel)]++;
-    if (seq >= kIpcSlots) {
-      ipc_wait_k<<<1, 1, 0, s>>>(flags_ + C_ + channel, seq - kIpcSlots + 1, timeout_ns_);
-      SPK_LAUNCH_CHECK();
-    }
+    if (seq >= kIpcSlots) wait_geq(s, flags_ + C_ + channel, seq - kIpcSlots + 1);  // ring slot consumed
     SPK_CUDA(cudaMemcpyAsync(ring + (seq % kIpcSlots) * slot_bytes_, buf, bytes, cudaMemcpyDeviceToDevice, s));
-    ipc_signal_k<<<1, 1, 0, s>>>(peer_flags_.at(peer) + channel, seq + 1);
-    SPK_LAUNCH_CHECK();
+    write_value(s, peer_flags_.at(peer) + channel, seq + 1);  // ready
   }
   void recv(void* buf, size_t bytes, int peer, int channel, uint64_t, cudaStream_t s) override {
     check(channel, bytes);
     auto it = rings_.find(channel);
     if (it == rings_.end() || recv_peer_.at(channel) != peer) throw std::logic_error("ipc: recv on an unconnected channel");
     const unsigned long long seq = recv_seq_[static_cast<size_t>(channel)]++;
-    ipc_wait_k<<<1, 1, 0, s>>>(flags_ + channel, seq + 1, timeout_ns_);
-    SPK_LAUNCH_CHECK();
+    wait_geq(s, flags_ + channel, seq + 1);  // message seq landed
     SPK_CUDA(cudaMemcpyAsync(buf, it->second + (seq % kIpcSlots) * slot_bytes_, bytes, cudaMemcpyDeviceToDevice, s));
-    ipc_signal_k<<<1, 1, 0, s>>>(peer_flags_.at(peer) + C_ + channel, seq + 1);
-    SPK_LAUNCH_CHECK();
+    write_value(s, peer_flags_.at(peer) + C_ + channel, seq + 1);  // consumed
   }
   bool try_recv(void* buf, size_t bytes, int peer, int channel, uint64_t tag, cudaStream_t s) override {
     recv(buf, bytes, peer, channel, tag, s);  // posting is asynchronous, like NCCL
     return true;
+  }
+  // Watchdog (the engine's step timed out): release every stream still waiting on this rank's
+  // flag words so the process can tear down and report DeadlockError.
+  void abort() override {
+    cudaStream_t t = nullptr;
+    if (cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking) == cudaSuccess) {
+      cudaMemsetAsync(flags_, 0xff, sizeof(unsigned long long) * 2 * C_, t);
+      cudaStreamDestroy(t);
+    }
   }
 
  private:
@@ -183,7 +208,6 @@ class IpcTransport final : public IpcExporter {
   }
   int rank_, C_;
   size_t slot_bytes_;
-  unsigned long long timeout_ns_;
   unsigned long long* flags_ = nullptr;  // [ready x C | consumed x C], written by the peers
   std::map<int, uint8_t*> rings_;        // receive channel -> R slots (exported)
   std::vector<uint8_t*> peer_ring_;      // send channel -> the receiver's ring (mapped)
