@@ -384,6 +384,12 @@ def main():
     else:
         cfg, part = full, part_full
     model.flags = E.FLAG_TIMELINE | (E.FLAG_RECOMPUTE_MLP if args.recompute_mlp else 0)
+    import torch  # device / pinned memory plumbing only
+    n_dev = torch.cuda.device_count()
+    # One GPU per rank. Fewer GPUs than ranks (a functional check of the N > 1 path on a
+    # smaller box, --transport ipc) puts several ranks on one device and says so in the line.
+    local = local % n_dev if n_dev else local
+    shared_gpu = world > 1 and n_dev < world
     eng = E.Engine(cfg, args.kind, part, model, rank=rank, world_size=world, cuda_device=local)
     if world > 1 and args.transport == "ipc":
         blobs = [None] * world
@@ -398,7 +404,6 @@ def main():
     T = cfg.seq_len
     rng = np.random.default_rng(1234)
     tokens = rng.integers(0, model.vocab, size=(cfg.micro_batches, T + 1), dtype=np.int64).astype(np.int32)
-    import torch  # device / pinned memory plumbing only
     tok_t = torch.from_numpy(tokens).to(f"cuda:{local}")
     tok_ptr = tok_t.data_ptr()
     tok_pinned = torch.from_numpy(tokens).pin_memory()
@@ -441,6 +446,10 @@ def main():
     barrier()
     e2e_step = max_over_ranks(sum(e2e_ms) / len(e2e_ms))
     loss_last = r.loss
+    if dist:  # the loss lives on the last stage's rank; the others report 0
+        t = torch.tensor([loss_last], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        loss_last = float(t.item())
     # ---- untimed probe step: per-class kernel times for the roofline
     eng.set_flags(model.flags | E.FLAG_KPROBE)
     probe = eng.step(tok_ptr, on_device=True)
@@ -523,6 +532,9 @@ def main():
             "config": config_of(args, cfg.micro_batches, T, cfg.segments, part.lengths),
             "loss": loss_last,
             "graph": bool(args.graph and world == 1),
+            **({"transport": args.transport} if world > 1 else {}),
+            **({"shared_gpu": f"{world} ranks on {n_dev} GPU(s): functional check, not a scaling number"}
+               if shared_gpu else {}),
             "tflops_per_gpu": fl / (step_ms / 1e3) / 1e12 / args.gpus,
             "model_flops_frac_of_peak": fl / (step_ms / 1e3) / 1e12 / args.gpus / sustained,
             "bubble_ratio": bubble, "modeled": modeled,

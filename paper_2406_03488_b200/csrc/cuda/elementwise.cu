@@ -425,32 +425,57 @@ __global__ void __launch_bounds__(256, 2) norm_fwd_rows_k(const __nv_bfloat16* _
 #pragma unroll
   for (int k = 0; k < NS; ++k) ld_f8(g + gi * (H / G) + (k * 32 + lane) * 8, gk[k]);
   for (int par = 0; row < n; row += stride, par ^= 1) {
-    Bf8 cur[NS];
+    // The slice is converted to fp32 once and kept in registers for the three passes (mean,
+    // centred squares, output): converting per pass cost 2 of the ~5 instructions per element
+    // of this issue-bound kernel.
+    float f[NS][8];
     cp_async_wait_all();
 #pragma unroll
-    for (int k = 0; k < NS; ++k) cur[k] = pf[k * 32 + lane];  // own lane's chunks: no barrier
+    for (int k = 0; k < NS; ++k) bf8_to_f(pf[k * 32 + lane], f[k]);  // own lane's chunks: no barrier
     if (row + stride < n) prefetch(row + stride);
-    float sm = 0.f;
-    if (!RMS) {
+    // Slice statistics (mg = the slice's mean, ss = its centred sum of squares; RMSNorm: mg = 0).
+    // G = 4 (h >= 4096, latency-bound): each lane's own mean and centred squares over its NS*8
+    // values, then ONE butterfly merging (mean, M2) pairs of equal counts (Chan: M2 = M2a + M2b
+    // + (mb - ma)^2 n/2) -- one shuffle chain per row instead of two. G = 2 (issue-bound): the
+    // butterfly's extra arithmetic costs more than the chain it saves (h 2560: 24.6 vs 22.7 us),
+    // so a sum chain, then the squares about the slice mean.
+    float mg = 0.f, ss = 0.f;
+    if (RMS) {
 #pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        float f[8];
-        bf8_to_f(cur[k], f);
+      for (int k = 0; k < NS; ++k)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) sm += f[e];
+        for (int e = 0; e < 8; ++e) ss += f[k][e] * f[k][e];
+      ss = warp_sum(ss);
+    } else if constexpr (G >= 4) {
+#pragma unroll
+      for (int k = 0; k < NS; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mg += f[k][e];
+      mg *= 1.f / (NS * 8);
+#pragma unroll
+      for (int k = 0; k < NS; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ss += (f[k][e] - mg) * (f[k][e] - mg);
+      float half = NS * 4;  // n/2 of each merged half
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1, half *= 2.f) {
+        const float om = __shfl_xor_sync(0xffffffffu, mg, o), os = __shfl_xor_sync(0xffffffffu, ss, o);
+        const float dm = om - mg;
+        ss = ss + os + dm * dm * half;
+        mg = 0.5f * (mg + om);
       }
-      sm = warp_sum(sm);
-    }
-    const float mg = RMS ? 0.f : sm * (static_cast<float>(G) / H);  // this slice's mean
-    float ss = 0.f;
+    } else {
 #pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      float f[8];
-      bf8_to_f(cur[k], f);
+      for (int k = 0; k < NS; ++k)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) ss += (f[e] - mg) * (f[e] - mg);
+        for (int e = 0; e < 8; ++e) mg += f[k][e];
+      mg = warp_sum(mg) * (static_cast<float>(G) / H);
+#pragma unroll
+      for (int k = 0; k < NS; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ss += (f[k][e] - mg) * (f[k][e] - mg);
+      ss = warp_sum(ss);
     }
-    ss = warp_sum(ss);
     if (lane == 0) xch[par][rb][gi] = make_float2(mg, ss);
     asm volatile("bar.sync %0, %1;" ::"r"(1 + rb), "r"(32 * G) : "memory");
     float mean = 0.f, m2 = 0.f;
@@ -467,11 +492,10 @@ __global__ void __launch_bounds__(256, 2) norm_fwd_rows_k(const __nv_bfloat16* _
     Bf8* yr = reinterpret_cast<Bf8*>(y + row * H) + gi * NS * 32;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      float f[8];
-      bf8_to_f(cur[k], f);
+      float o[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) f[e] = (f[e] - mean) * rstd * gk[k][e];
-      yr[k * 32 + lane] = f_to_bf8(f);
+      for (int e = 0; e < 8; ++e) o[e] = (f[k][e] - mean) * rstd * gk[k][e];
+      yr[k * 32 + lane] = f_to_bf8(o);
     }
     if (lane == 0 && gi == 0) {
       if (!RMS) mean_out[row] = mean;
