@@ -37,6 +37,24 @@ struct __align__(64) TcParams {
   int num_m_blk, num_n_blk, num_k_blk;
 };
 
+// Tile raster of the persistent kernels: groups of kGroupM m-blocks, n-blocks walked inside a
+// group. The CTAs of one wave (consecutive tiles) then share ~8 A and ~10 B panels instead of
+// every A panel of the matrix (m fastest): at the cfg-2 shapes the wave's operand set fits in
+// L2 and each panel comes from DRAM about once per wave (ncu: 1.27 GB of DRAM reads for a
+// 10170 x 2560 x 10240 GEMM whose operands are 0.26 GB).
+#ifndef SPK_GEMM_GROUP_M
+#define SPK_GEMM_GROUP_M 8  // tools/build_variant.py -DSPK_GEMM_GROUP_M=1000 reproduces the m-fastest raster
+#endif
+constexpr int kGroupM = SPK_GEMM_GROUP_M;
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
+  const int per_group = kGroupM * num_n;
+  const int g = tile / per_group, r = tile - g * per_group;
+  const int m0 = g * kGroupM;
+  const int gm = num_m - m0 < kGroupM ? num_m - m0 : kGroupM;
+  mb = m0 + r % gm;
+  nb = r / gm;
+}
+
 template <typename TC>
 __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t row, int64_t col0, const uint32_t (&r)[32]) {
   TC* C;
@@ -156,7 +174,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_k(const __grid_constan
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
+        int mb, nb;
+        tile_coords(tile, p.num_m_blk, p.num_n_blk, mb, nb);
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           tc::mbar_expect_tx(&full[stage], STAGE_BYTES);
@@ -223,7 +242,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_k(const __grid_constan
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
+      int mb, nb;
+        tile_coords(tile, p.num_m_blk, p.num_n_blk, mb, nb);
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::tc_fence_after();
       const int64_t row = (int64_t)mb * BM + quarter * 32 + lane;
@@ -322,7 +342,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc2_k(const __grid_consta
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cid; tile < num_tiles; tile += ncl) {
-        const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
+        int mb, nb;
+        tile_coords(tile, p.num_m_blk, p.num_n_blk, mb, nb);
         const int m0 = mb * 256 + static_cast<int>(rank) * BM2, n0 = nb * 256 + static_cast<int>(rank) * BNH;
         for (int kb = 0; kb < p.num_k_blk; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
@@ -406,7 +427,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc2_k(const __grid_consta
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = cid; tile < num_tiles; tile += ncl) {
-      const int mb = tile % p.num_m_blk, nb = tile / p.num_m_blk;
+      int mb, nb;
+        tile_coords(tile, p.num_m_blk, p.num_n_blk, mb, nb);
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::tc_fence_after();
       const int64_t row = (int64_t)mb * 256 + rank * BM2 + quarter * 32 + lane;
