@@ -44,6 +44,26 @@ inline int num_sms() {
 #if defined(__CUDACC__)
 namespace spk {
 
+// tanh-form GeLU derivative, shared by the activation kernels and the GEMM epilogue that
+// fuses the MLP activation backward (Epi::kGeluGrad). Exact form (libm tanhf, the fp32
+// validation path) and the bf16 production form (MUFU tanh.approx.f32, rel. error ~2^-11,
+// below the bf16 output rounding).
+__device__ __forceinline__ float gelu_tanh_grad(float u) {
+  const float c = 0.7978845608028654f;
+  const float t = tanhf(c * (u + 0.044715f * u * u * u));
+  return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * u * u);
+}
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu_grad_fast(float u) {
+  const float c = 0.7978845608028654f;
+  const float t = tanh_fast(c * (u + 0.044715f * u * u * u));
+  return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * u * u);
+}
+
 template <typename T>
 __device__ __forceinline__ float to_f(T v);
 template <>

@@ -128,11 +128,6 @@ __device__ __forceinline__ float gelu_tanh(float u) {
   const float c = 0.7978845608028654f;
   return 0.5f * u * (1.f + tanhf(c * (u + 0.044715f * u * u * u)));
 }
-__device__ __forceinline__ float gelu_tanh_grad(float u) {
-  const float c = 0.7978845608028654f;
-  const float t = tanhf(c * (u + 0.044715f * u * u * u));
-  return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * u * u);
-}
 __device__ __forceinline__ float sigmoidf_(float u) { return 1.f / (1.f + expf(-u)); }
 
 template <typename T>
@@ -778,19 +773,9 @@ __device__ __forceinline__ float gelu_f(float u) { return gelu_tanh(u); }
 // bf16 production path: MUFU tanh (tanh.approx.f32, max rel. error ~2^-11, far
 // below the bf16 output rounding). libm tanhf made these HBM-sized kernels
 // issue-bound (~20 instructions per element). The fp32 validation path keeps tanhf.
-__device__ __forceinline__ float tanh_fast(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 __device__ __forceinline__ float gelu_fast(float u) {
   const float c = 0.7978845608028654f;
   return 0.5f * u * (1.f + tanh_fast(c * (u + 0.044715f * u * u * u)));
-}
-__device__ __forceinline__ float gelu_grad_fast(float u) {
-  const float c = 0.7978845608028654f;
-  const float t = tanh_fast(c * (u + 0.044715f * u * u * u));
-  return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * u * u);
 }
 __device__ __forceinline__ float sigmoid_fast(float u) { return fmaf(0.5f, tanh_fast(0.5f * u), 0.5f); }
 

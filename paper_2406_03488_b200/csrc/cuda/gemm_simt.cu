@@ -86,6 +86,8 @@ __global__ void __launch_bounds__(256) gemm_simt_k(GemmArgs a) {
         v += to_f(C[idx]);
       } else if (a.epi == Epi::kAddResid) {
         v += to_f(static_cast<const TC*>(a.R)[gm * a.ldr + gn]);
+      } else if (a.epi == Epi::kGeluGrad) {
+        v *= gelu_tanh_grad(to_f(static_cast<const TC*>(a.R)[gm * a.ldr + gn]));
       }
       C[idx] = from_f<TC>(v);
     }

@@ -102,6 +102,26 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t row, int6
       for (int j = 0; j < 32 && col0 + j < g.N; ++j) v[j] += to_f(R[j]);
     }
   }
+  if (g.epi == Epi::kGeluGrad) {  // bf16 C only (gemm_tc_supported)
+    const TC* R = static_cast<const TC*>(g.R) + row * g.ldr + col0;
+    if (full) {
+      if constexpr (sizeof(TC) == 2) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u = reinterpret_cast<const uint4*>(R)[q];
+          const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float2 f = __bfloat1622float2(b[e]);
+            v[q * 8 + 2 * e] *= gelu_grad_fast(f.x);
+            v[q * 8 + 2 * e + 1] *= gelu_grad_fast(f.y);
+          }
+        }
+      }
+    } else {
+      for (int j = 0; j < 32 && col0 + j < g.N; ++j) v[j] *= gelu_grad_fast(to_f(R[j]));
+    }
+  }
   if (g.epi == Epi::kAccumF32) {
     if (full) {
 #pragma unroll
@@ -493,6 +513,7 @@ bool gemm_tc_supported(const GemmArgs& a) {
   const int cvec = a.c == DType::kF32 ? 4 : 8;
   if (a.ldc % cvec || !aligned16(a.C)) return false;
   if (a.epi == Epi::kAddResid && (a.ldr % cvec || !aligned16(a.R))) return false;
+  if (a.epi == Epi::kGeluGrad && (a.c != DType::kBF16 || a.ldr % 8 || !aligned16(a.R))) return false;
   if (a.split_n >= 0 && (a.split_n % 32 || a.ldc2 % cvec || !aligned16(a.C2))) return false;
   return true;
 }

@@ -18,6 +18,7 @@ enum class Epi : int {
   kStore = 0,     // C = acc                     (cast to c dtype)
   kAccumF32 = 1,  // C += acc                    (fp32 C: weight-gradient accumulation)
   kAddResid = 2,  // C = acc + R                 (residual stream; R may alias C)
+  kGeluGrad = 3,  // C = acc * gelu'(R)          (MLP dgrad fused with the GeLU backward; R = u)
 };
 
 struct GemmArgs {

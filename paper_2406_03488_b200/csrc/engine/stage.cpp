@@ -697,17 +697,35 @@ void Stage::backward_impl(int m, int s, void* dx_target, const int32_t* tokens, 
       g.epi = Epi::kAccumF32;
       wgrad(g, 2.0 * n * h * F);
     }
-    gemm(G(dt, n, F, h, dy, h, true, wc(w.w2), F, false, w_big2_, F, dt), 2.0 * n * h * F);
-    join();  // act_bwd overwrites w_big1_
-    spk::act_bwd(dt, mc_.family, u, w_big2_, w_big1_, n, F, s_);
+    void* du = w_big1_;
+    static const bool fuse_gelu_bwd = [] {
+      const char* e = std::getenv("SP_FUSE_GELU_BWD");  // tuning: 0 = dgrad GEMM + elementwise GeLU backward
+      return e ? std::atoi(e) != 0 : true;
+    }();
+    if (mc_.family == SP_MODEL_GPT && fuse_gelu_bwd) {
+      // GeLU: du = (dy W2) * gelu'(u) straight from the dgrad GEMM's epilogue into w_big2_ --
+      // no dg round trip through HBM, no activation-backward launch, and no wait for the W2
+      // weight gradient (still reading g from w_big1_ on the side stream).
+      g = G(dt, n, F, h, dy, h, true, wc(w.w2), F, false, w_big2_, F, dt);
+      g.epi = Epi::kGeluGrad;
+      g.R = u;
+      g.ldr = Fu;
+      gemm(g, 2.0 * n * h * F);
+      du = w_big2_;
+    } else {  // SwiGLU (du has two halves per row) or the unfused GeLU: the elementwise backward
+      gemm(G(dt, n, F, h, dy, h, true, wc(w.w2), F, false, w_big2_, F, dt), 2.0 * n * h * F);
+      join();  // act_bwd overwrites w_big1_
+      spk::act_bwd(dt, mc_.family, u, w_big2_, w_big1_, n, F, s_);
+      ++launches;
+    }
     if (defer_w) {
-      SPK_CUDA(cudaMemcpyAsync(sg.w_du[l], w_big1_, esz_ * n * Fu, cudaMemcpyDeviceToDevice, s_));
+      SPK_CUDA(cudaMemcpyAsync(sg.w_du[l], du, esz_ * n * Fu, cudaMemcpyDeviceToDevice, s_));
     } else {
-      g = G(dt, Fu, h, n, w_big1_, Fu, false, w_a_, h, false, wg(w.w1), h, DType::kF32);
+      g = G(dt, Fu, h, n, du, Fu, false, w_a_, h, false, wg(w.w1), h, DType::kF32);
       g.epi = Epi::kAccumF32;
       wgrad(g, 2.0 * n * Fu * h);
     }
-    gemm(G(dt, n, h, Fu, w_big1_, Fu, true, wc(w.w1), h, false, w_t1_, h, dt), 2.0 * n * Fu * h);
+    gemm(G(dt, n, h, Fu, du, Fu, true, wc(w.w1), h, false, w_t1_, h, dt), 2.0 * n * Fu * h);
     join();
     spk::norm_bwd(dt, mc_.rms(), w_t1_, sg.x_mid[l], wm(w.norm2), sg.mean2[l], sg.rstd2[l], dy, w_t2_, wg(w.norm2), n,
                   mc_.h, s_);
@@ -750,7 +768,7 @@ void Stage::backward_impl(int m, int s, void* dx_target, const int32_t* tokens, 
     spk::norm_bwd(dt, mc_.rms(), w_t1_, sg.x_in[l], wm(w.norm1), sg.mean1[l], sg.rstd1[l], w_t2_, dx, wg(w.norm1), n,
                   mc_.h, s_);
     dy = w_t2_;
-    launches += 8;
+    launches += 7;  // norm_apply x2, act_fwd, norm_bwd x2, attn_bwd, assemble_dqkv
   }
   if (first()) {
     spk::embed_bwd(dt, tokens + (int64_t)(m - 1) * (T_ + 1) + pos0, w_t3_, wg(embed_), pos_ >= 0 ? wg(pos_) : nullptr,
