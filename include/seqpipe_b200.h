@@ -336,8 +336,11 @@ int sp_engine_comm_init(sp_engine* eng, const uint8_t* const* ids, int32_t n_ids
  * sp_engine_ipc_export (size query with out == NULL, then the copy; it allocates the rank's
  * receive rings and flag words once), the blobs travel over any side channel, then every rank
  * calls sp_engine_ipc_connect with all of them in rank order. A message is one device-to-device
- * copy into the receiver's ring plus a release / acquire flag pair; a transfer that never pairs
- * up traps the CUDA context after the engine's watchdog time. */
+ * copy into the receiver's ring plus two flag words, written and awaited by the streams
+ * themselves (cuStreamWriteValue64 / cuStreamWaitValue64: no SM spins). A transfer that never
+ * pairs up: sp_engine_step returns SP_ERR_DEADLOCK after the watchdog time (SP_P2P_WATCHDOG_S);
+ * the engine is then unusable (later steps fail the same way) and sp_engine_destroy releases it
+ * without waiting on the parked streams, so the process can exit. */
 int sp_engine_ipc_export(sp_engine* eng, uint8_t* out, size_t* len);
 int sp_engine_ipc_connect(sp_engine* eng, const uint8_t* const* blobs, const size_t* lens, int32_t n);
 int sp_local_hub_create(int32_t world_size, double watchdog_seconds, sp_local_hub** out);

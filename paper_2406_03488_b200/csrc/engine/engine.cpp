@@ -156,6 +156,15 @@ Engine::Engine(const seqpipe::ScenarioConfig& cfg, seqpipe::ScheduleKind kind, c
 
 Engine::~Engine() {
   cudaSetDevice(dev_);
+  if (poisoned_) {
+    // After a P2P watchdog: streams may stay parked on a peer that will never answer. Leak the
+    // device state instead of blocking in a synchronize or an implicitly synchronizing free;
+    // the process is expected to exit (the reference raises DeadlockError and stops too).
+    for (auto& [v, st] : stages_) (void)st.release();
+    (void)transport_.release();
+    (void)cudaGetLastError();
+    return;
+  }
   if (s_) cudaStreamSynchronize(s_);
   for (auto& [c, st] : send_s_) cudaStreamSynchronize(st);
   for (auto& [c, rc] : recv_ch_) cudaStreamSynchronize(rc.s);
@@ -439,6 +448,8 @@ void Engine::enable_graph(bool on) {
 }
 
 void Engine::step(const int32_t* tokens, bool on_device, sp_step_report* rep) {
+  if (poisoned_)
+    throw seqpipe::DeadlockError("engine unusable after a P2P watchdog timeout: destroy it and restart the job");
   SPK_CUDA(cudaSetDevice(dev_));
   if (world_ > 1 && !transport_)
     throw std::logic_error("multi-rank engine: call sp_engine_comm_init / sp_engine_attach_local first");
@@ -508,6 +519,7 @@ void Engine::step(const int32_t* tokens, bool on_device, sp_step_report* rep) {
       if (q != cudaErrorNotReady) SPK_CUDA(q);
       if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > watchdog_s_) {
         transport_->abort();
+        poisoned_ = true;
         throw seqpipe::DeadlockError("P2P watchdog: step of rank " + std::to_string(rank_) + " did not complete in " +
                                      std::to_string(watchdog_s_) + " s");
       }

@@ -304,6 +304,10 @@ class Engine {
   cudaEvent_t ev_step0_ = nullptr, ev_step1_ = nullptr;
   std::vector<double> t_start_, t_end_;
   std::unique_ptr<Transport> transport_;
+  // Set when the P2P watchdog fired and the transport could not release every parked stream
+  // wait: device work may never retire, so teardown must neither synchronize nor free memory
+  // that work can still touch (cudaFree synchronizes the device).
+  bool poisoned_ = false;
   std::vector<void*> send_ring_;
   std::vector<cudaEvent_t> send_ring_ev_;
   int send_ring_next_ = 0;

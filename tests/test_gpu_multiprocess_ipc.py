@@ -96,3 +96,53 @@ def test_multiprocess_ipc_step_matches_reference_order_and_oracle(gpu, kind, P, 
     assert abs(res[P - 1]["loss"] - loss) / abs(loss) < tol, (res[P - 1]["loss"], loss)
     bad = {n: rel_l2(grads_eng[n], grads[n]) for n in params}
     assert max(bad.values()) < tol, bad
+
+
+def _deadlock_worker(rank, world, port, out_dir):
+    os.environ["SP_P2P_WATCHDOG_S"] = "5"  # read when the engine is created
+    import time
+
+    import torch.distributed as dist
+
+    from oracle.transformer import GPT, tokens_for
+    from paper_2406_03488_b200 import engine as E
+    from paper_2406_03488_b200 import planner as pl
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    model = _model(E, GPT, world, False)
+    cfg = pl.ScenarioConfig(pipeline_size=world, micro_batches=2 * world, segments=2, seq_len=512,
+                            layers=model.layers, hidden_dim=model.hidden, param_count=model.param_count())
+    eng = E.Engine(cfg, "seq1f1b", pl.partition_for(cfg, "cwp"), model, rank=rank, world_size=world, cuda_device=0)
+    blobs = [None] * world
+    dist.all_gather_object(blobs, eng.ipc_export())
+    eng.ipc_connect(blobs)
+    res = {"rank": rank}
+    if rank == 0:  # rank 1 never steps: rank 0's first receive can never pair up
+        t0 = time.time()
+        try:
+            eng.step(tokens_for(cfg.micro_batches, cfg.seq_len, model.vocab, seed=5))
+            res["error"] = None
+        except pl.DeadlockError as e:
+            res["error"] = str(e)
+        res["seconds"] = time.time() - t0
+    with open(os.path.join(out_dir, f"rank{rank}.pkl"), "wb") as f:
+        pickle.dump(res, f)
+    dist.barrier()
+    eng.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_multiprocess_ipc_watchdog_turns_a_missing_peer_into_deadlock_error(gpu):
+    """The reference's failure mode for a transfer that never pairs up (sim.cpp:217-231,
+    DeadlockError) on the peer-memory transport: rank 1 never runs its step, rank 0's step
+    raises DeadlockError after the watchdog (its parked stream waits are released) instead of
+    hanging, and both processes tear down cleanly."""
+    import torch.multiprocessing as mp
+
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_deadlock_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        with open(os.path.join(d, "rank0.pkl"), "rb") as f:
+            r0 = pickle.load(f)
+    assert r0["error"] and "watchdog" in r0["error"], r0
+    assert 4.0 < r0["seconds"] < 60.0, r0

@@ -24,10 +24,10 @@ def gdb_dump(rank):
     log(rank, f"gdb dump -> {out}")
 
 
-def worker(rank, world, port, kind, k, bf16, steps):
+def worker(rank, world, port, kind, k, bf16, steps, idle_rank=-1):
     import threading
     faulthandler.dump_traceback_later(150, exit=True)
-    t = threading.Timer(45, gdb_dump, args=(rank,))
+    t = threading.Timer(float(os.environ.get("IPC_DBG_GDB_S", "45")), gdb_dump, args=(rank,))
     t.daemon = True
     t.start()
     import torch.distributed as dist
@@ -57,17 +57,23 @@ def worker(rank, world, port, kind, k, bf16, steps):
     log(rank, "connected")
     dist.barrier()
     tok = tokens_for(cfg.micro_batches, cfg.seq_len, model.vocab, seed=5)
+    if rank == idle_rank:  # never steps: the peers' transfers with this rank cannot pair up
+        log(rank, "idle (not stepping)")
+        steps = 0
     for i in range(steps):
         t0 = time.time()
         try:
             rep = eng.step(tok)
             log(rank, f"step {i}: loss {rep.loss:.6f} in {time.time() - t0:.3f} s")
         except Exception as e:  # noqa: BLE001
-            log(rank, f"step {i} FAILED after {time.time() - t0:.1f} s: {e}")
-            os._exit(3)
-    t.cancel()
+            log(rank, f"step {i} FAILED after {time.time() - t0:.1f} s: {type(e).__name__}: {e}")
+            if idle_rank < 0:
+                os._exit(3)
+            break
+    log(rank, "closing")
     eng.close()
     log(rank, "closed")
+    t.cancel()
     dist.barrier()
     dist.destroy_process_group()
 
@@ -79,12 +85,13 @@ def main():
     ap.add_argument("--kind", default="seq1f1b")
     ap.add_argument("--bf16", action="store_true")
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--idle-rank", type=int, default=-1, help="this rank never steps (watchdog check)")
     a = ap.parse_args()
     import torch.multiprocessing as mp
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    mp.spawn(worker, args=(a.P, port, a.kind, a.k, a.bf16, a.steps), nprocs=a.P, join=True)
+    mp.spawn(worker, args=(a.P, port, a.kind, a.k, a.bf16, a.steps, a.idle_rank), nprocs=a.P, join=True)
     print("ok", file=sys.stderr)
 
 
