@@ -75,7 +75,7 @@ def peaks():
 def traffic_of(kernel):
     """DRAM bytes per launch of the dominant kernel class from the committed ncu capture."""
     try:
-        d = json.loads((ROOT / "profiles" / "r1_traffic.json").read_text())[kernel]
+        d = json.loads((ROOT / "profiles" / "r2_traffic.json").read_text())[kernel]
         return d["dram_bytes_per_launch"], d["launch"]
     except Exception:
         return None, None
